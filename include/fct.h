@@ -1,0 +1,174 @@
+/*
+ * fct.h -- C ABI of libfct.so: the B200 (sm_100a) hot path of the Fast Cauchy Transform
+ * l1-conditioning pipeline of Clarkson, Drineas, Magdon-Ismail, Mahoney, Meng, Woodruff,
+ * "The Fast Cauchy Transform and Faster Robust Linear Regression" (arXiv 1207.4684).
+ * Citations "P:L<n>" are lines of that paper's text; DESIGN.md lists the readings
+ * taken where the paper is silent.
+ *
+ * Conventions (all entry points):
+ *  - Matrices are row-major.  A is n x d with leading dimension lda (>= d), fp32.
+ *  - Unless an argument is documented as HOST memory, every pointer is a DEVICE pointer owned
+ *    by the caller.  The library allocates no device memory: scratch space is the caller's
+ *    `workspace` (size from the matching *_workspace_bytes query, 256-byte aligned).
+ *  - `stream` is a cudaStream_t (NULL = the legacy default stream).  All device work is
+ *    enqueued asynchronously on it; argument validation is synchronous and happens before
+ *    anything is enqueued, so a non-OK return means nothing was enqueued.
+ *  - Return value: FCT_OK or a negative fct_status; fct_last_error() gives a message
+ *    (thread-local).  Asynchronous device faults surface at the next synchronising call
+ *    (CUDA semantics).  No C++ exception crosses this boundary.  Functions are re-entrant;
+ *    the library keeps no global state besides the thread-local error string and a
+ *    per-device cache of kernel attributes.
+ *  - Setting the environment variable FCT_DEBUG=1 synchronises after every launch and
+ *    range-checks hash_rows (slow; for debugging).
+ */
+#ifndef FCT_H_
+#define FCT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int fct_status;
+enum {
+  FCT_OK = 0,
+  FCT_ERR_ARG = -1,         /* bad scalar argument or NULL pointer                           */
+  FCT_ERR_SHAPE = -2,       /* inconsistent sizes (n < 1, d < 1, lda < d, r1 < 1, r1 < d ...) */
+  FCT_ERR_CUDA = -3,        /* a CUDA launch/runtime error                                   */
+  FCT_ERR_CAPACITY = -4,    /* a host-side result does not fit the caller's buffer           */
+  FCT_ERR_SINGULAR = -5,    /* Cholesky of Y^T Y broke down (host-synchronous entry points)  */
+  FCT_ERR_UNSUPPORTED = -6, /* no kernel instance for these sizes                            */
+  FCT_ERR_WORKSPACE = -7    /* workspace NULL or smaller than the *_workspace_bytes query    */
+};
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* fct_last_error(void);
+/* Library version string, e.g. "fct-b200 0.1 sm_100a". */
+const char* fct_version(void);
+
+/* Limits of this build. */
+#define FCT_MAX_S 4096   /* Hadamard block size s: power of two in [1, FCT_MAX_S]          */
+#define FCT_MAX_D 128    /* columns handled by fct_condition / l1_rownorm                  */
+#define FCT_MAX_K 32     /* r2 = k, the number of Cauchy columns of Pi2                    */
+
+/* ------------------------------------------------------------------------------------------
+ * FCT1 sketch (Sec. 3.1; Thm FCT1):
+ *     Y (r1 x d, ld = d, fp32)  :=  [accumulate ? Y : 0]  +  4 * B * C * H~ * D * A_pad
+ * with A_pad = A zero-padded to n' = s*ceil(n/s) rows (P:L2255-2256 assumes s | n).
+ *   signs[n]        D, the Rademacher diagonal (+1/-1), int8 (north_star addition; D = I gives
+ *                   the paper's Pi1 = 4 B C H~ exactly).
+ *   cauchy_diag[2n'] diag(C), i.i.d. standard Cauchy, fp32, indexed by H~-row.
+ *   hash_rows[2n']  B: column t of B is e_{hash_rows[t]}, values in [0, r1).
+ *   H~ row layout: block b occupies H~-rows [2sb, 2sb+2s); row 2sb+r (r < s) is row r of the
+ *   normalised Hadamard H_s = H/sqrt(s) (Sylvester order) applied to block b,
+ *   row 2sb+s+r is row r of I_s (G_s = [H_s; I_s]).
+ * s must be a power of two in [1, FCT_MAX_S].
+ * Row shards: call with A + row0*lda, signs + row0, cauchy_diag + 2*row0, hash_rows + 2*row0
+ * (row0 % s == 0) and accumulate = 1 to add the shard's contribution (Pi1 A = sum of shards).
+ * Accuracy: partial sums are kept in fp32 in shared memory for <= 4096 terms per bucket and
+ * then accumulated in fp64 (workspace); |Y - exact| <= 1e-5 * (4|B||C||H~||D||A|) entrywise.
+ * Y may be written by any order of floating-point additions (run-to-run bitwise variation).
+ */
+size_t fct_sketch_workspace_bytes(int64_t n, int64_t d, int32_t s, int32_t r1);
+fct_status fct_sketch(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs,
+                      const float* cauchy_diag, const int32_t* hash_rows, int32_t s, int32_t r1,
+                      float* Y, int accumulate, void* workspace, size_t workspace_bytes,
+                      void* stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Conditioning (FastL1Basis): R with Y = Q R, Q orthonormal columns, diag(R) > 0
+ * (unique; reading R19), computed by CholeskyQR2 in fp64, and Rinv = R^-1
+ * (O(r1 d^2) + O(d^3)).  Y: r1 x d fp32 (the sketch); R, Rinv: d x d fp64
+ * row-major (upper triangular).  info (device int32): 0 on success, j+1 if the j-th pivot
+ * of the Cholesky factorisation was not positive/finite (rank-deficient Y).
+ * Requires 1 <= d <= FCT_MAX_D and r1 >= d.
+ */
+size_t fct_condition_workspace_bytes(int32_t r1, int64_t d);
+fct_status fct_condition(const float* Y, int32_t r1, int64_t d, double* R, double* Rinv,
+                         int32_t* info, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------
+ * l1 row-norm estimation (Lemma medCauchy, cost P:L2168-2175):
+ *     M = Rinv * Pi2 (formed first, fp64);  Lambda = A M;
+ *     lambda[i] = median_j |Lambda_ij|   (even k: mean of the two middle order statistics)
+ *     *lambda_sum += sum_i lambda[i]      (fp64 device scalar, fixed summation order)
+ * Rinv: d x d fp64; Pi2: d x k fp32 (i.i.d. Cauchy); lambda: n fp32.
+ * Accuracy: |lambda - exact| <= 1e-5 * exact per row.  Rows whose fp32 evaluation cannot be
+ * certified to that bound (cancellation) are recomputed in fp64 inside the kernel.
+ * Requires 1 <= d <= FCT_MAX_D, 1 <= k <= FCT_MAX_K.
+ */
+size_t l1_rownorm_workspace_bytes(int64_t n, int64_t d, int32_t k);
+fct_status l1_rownorm(const float* A, int64_t n, int64_t d, int64_t lda, const double* Rinv,
+                      const float* Pi2, int32_t k, float* lambda, double* lambda_sum,
+                      void* workspace, size_t workspace_bytes, void* stream);
+/* p[i] = (float)((double)lambda[i] / *lambda_total)   (t_i of P:L2028-2033). */
+fct_status l1_probs(const float* lambda, int64_t n, const double* lambda_total, float* p,
+                    void* stream);
+/* Single-device convenience: l1_rownorm (with a zeroed local sum) followed by l1_probs.
+ * lambda_sum (device fp64, may be NULL) receives the total. */
+fct_status l1_rownorm_probs(const float* A, int64_t n, int64_t d, int64_t lda,
+                            const double* Rinv, const float* Pi2, int32_t k, float* lambda,
+                            float* p, double* lambda_sum, void* workspace,
+                            size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Bernoulli l1 sampling (l1 sampling lemma P:L1258-1268 with s := m):
+ *     phat_i = min(1, m * (double)p[i])   (exact in fp64 for m <= 2^29)
+ *     keep row i  iff  u_i < phat_i,  u_i = u53(rng_u64(seed, 9, row_base + i))
+ *     idx[]    = kept GLOBAL row indices row_base + i, strictly increasing (int64)
+ *     weight[] = 1.0 / phat_i (fp64, IEEE division)        -- D_ii = 1/phat_i
+ *     *count   = number kept (device int64; may exceed capacity: only the first `capacity`
+ *                entries are written -- compare on the host).
+ * rng_u64(seed, stream, i) = mix64(mix64(seed + G(stream+1)) + G(i+1)), G = 0x9E3779B97F4A7C15,
+ * mix64 = SplitMix64 finaliser; u53(x) = (x >> 11) * 2^-53.  Recommended capacity: 2m + 64
+ * (S <= 2s w.p. >= 1 - e^{-3s/8}).  Bit-exact given p and the uniforms.
+ */
+size_t l1_sample_workspace_bytes(int64_t n);
+fct_status l1_sample(const float* p, int64_t n, int64_t row_base, int64_t m, uint64_t seed,
+                     int64_t* idx, double* weight, int64_t capacity, int64_t* count,
+                     void* workspace, size_t workspace_bytes, void* stream);
+/* Same with explicit uniforms u[n] in [0,1) (device fp64) instead of the generator. */
+fct_status l1_sample_u(const float* p, const double* u, int64_t n, int64_t row_base,
+                       int64_t m, int64_t* idx, double* weight, int64_t capacity,
+                       int64_t* count, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Whole single-device hot path: sketch -> condition -> row-norm ->
+ * probabilities -> sample, all enqueued on `stream` (device pointers).  Y (r1 x d fp32),
+ * R, Rinv (d x d fp64), lambda, p (n fp32), idx/weight (capacity), count, info are outputs.
+ */
+size_t fct_pipeline_workspace_bytes(int64_t n, int64_t d, int32_t s, int32_t r1, int32_t k);
+fct_status fct_pipeline(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs,
+                        const float* cauchy_diag, const int32_t* hash_rows, int32_t s,
+                        int32_t r1, const float* Pi2, int32_t k, int64_t m, uint64_t seed,
+                        float* Y, double* R, double* Rinv, float* lambda, float* p,
+                        int64_t* idx, double* weight, int64_t capacity, int64_t* count,
+                        int32_t* info, void* workspace, size_t workspace_bytes, void* stream);
+
+/* The same pipeline from HOST buffers (end-to-end entry point).  A_host, signs_host,
+ * cauchy_host, hash_host, Pi2_host are HOST pointers (pinned memory recommended); the inputs
+ * are copied in s-aligned chunks on `stream` while the sketch of earlier chunks runs.
+ * dev_A (n x lda fp32), dev_aux (fct_pipeline_aux_bytes) are caller-owned device buffers
+ * that receive the inputs.  Outputs idx_host/weight_host (capacity), *count_host are HOST
+ * memory; the call returns after they are valid (it synchronises `stream`).  Device copies of
+ * Y, R, Rinv, lambda, p live in the workspace-derived buffers of fct_pipeline and are
+ * discarded.  Returns FCT_ERR_CAPACITY if count > capacity (count still written),
+ * FCT_ERR_SINGULAR if the conditioning failed.
+ */
+size_t fct_pipeline_aux_bytes(int64_t n, int64_t d, int32_t s, int32_t k);
+size_t fct_pipeline_host_workspace_bytes(int64_t n, int64_t d, int32_t s, int32_t r1, int32_t k,
+                                         int64_t capacity);
+fct_status fct_pipeline_host(const float* A_host, int64_t n, int64_t d, int64_t lda,
+                             const int8_t* signs_host, const float* cauchy_host,
+                             const int32_t* hash_host, int32_t s, int32_t r1,
+                             const float* Pi2_host, int32_t k, int64_t m, uint64_t seed,
+                             int64_t* idx_host, double* weight_host, int64_t capacity,
+                             int64_t* count_host, float* dev_A, void* dev_aux,
+                             void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FCT_H_ */

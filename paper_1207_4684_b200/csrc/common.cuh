@@ -1,0 +1,80 @@
+// common.cuh -- shared helpers of libfct.so (error plumbing, workspace carving, launch checks).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdarg.h>
+#include <algorithm>
+#include <stdlib.h>
+
+#include "../../include/fct.h"
+
+namespace fct {
+
+// thread-local last-error message (fct_last_error)
+void set_error(const char* fmt, ...);
+const char* get_error();
+bool debug_sync();  // FCT_DEBUG=1
+
+#define FCT_CHECK_ARG(cond, code, ...)          \
+  do {                                          \
+    if (!(cond)) {                              \
+      ::fct::set_error(__VA_ARGS__);            \
+      return (code);                            \
+    }                                           \
+  } while (0)
+
+#define FCT_CUDA_RET(expr)                                                                  \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      ::fct::set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return FCT_ERR_CUDA;                                                                  \
+    }                                                                                       \
+  } while (0)
+
+// after a launch: catch configuration errors; in debug mode also synchronise
+inline fct_status post_launch(const char* what, cudaStream_t st) {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && debug_sync()) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return FCT_ERR_CUDA;
+  }
+  return FCT_OK;
+}
+#define FCT_LAUNCHED(what, st)                     \
+  do {                                             \
+    fct_status s_ = ::fct::post_launch(what, st);  \
+    if (s_ != FCT_OK) return s_;                   \
+  } while (0)
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// sequential carving of a caller workspace into 256-byte aligned pieces
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* p) : base((char*)p) {}
+  template <class T> T* take(size_t count) {
+    T* p = base ? (T*)(base + off) : nullptr;
+    off += align256(count * sizeof(T));
+    return p;
+  }
+};
+
+inline int num_sms() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+inline bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+
+}  // namespace fct
+
+// internal entry points used by the pipeline (same validation as the public ones)
+fct_status fct_rownorm_impl(const float* A, int64_t n, int64_t d, int64_t lda, const double* Rinv,
+                            const float* Pi2, int32_t k, float* lambda, double* lambda_sum,
+                            bool zero_sum, void* ws, size_t wsb, cudaStream_t st);

@@ -1,0 +1,66 @@
+"""The C ABI library loads and exports every symbol include/fct.h declares (no GPU needed)."""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "fct.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+char\s*\*|size_t|fct_status)\s+(\w+)\s*\(", src, flags=re.M)
+    return sorted(set(names))
+
+
+@pytest.fixture(scope="module")
+def libpath():
+    from paper_1207_4684_b200 import build
+    try:
+        return build.build()
+    except (OSError, subprocess.CalledProcessError) as e:   # no nvcc here: nothing to check
+        pytest.skip(f"cannot build libfct.so: {e}")
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ("fct_sketch", "l1_rownorm_probs", "l1_sample", "l1_rownorm", "l1_probs", "fct_condition",
+                 "fct_last_error", "fct_pipeline", "fct_pipeline_host"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(libpath):
+    out = subprocess.check_output(["nm", "-D", "--defined-only", libpath], text=True)
+    exported = {ln.split()[-1] for ln in out.splitlines() if ln.strip()}
+    missing = [n for n in declared_functions() if n not in exported]
+    assert not missing, missing
+
+
+def test_binding_signatures_match_header(libpath):
+    from paper_1207_4684_b200 import _lib
+    assert set(_lib.SIGNATURES) == set(declared_functions())
+    lib = _lib.load()
+    assert lib.fct_version().decode().startswith("fct-b200")
+
+
+def test_host_side_validation_without_gpu(libpath):
+    """Argument validation is synchronous and needs no device: bad calls fail with the documented codes."""
+    from paper_1207_4684_b200 import _lib
+    lib = _lib.load()
+    # NULL pointers -> FCT_ERR_ARG
+    assert lib.fct_sketch(None, 10, 2, 2, None, None, None, 4, 4, None, 0, None, 0, None) == -1
+    assert b"NULL" in lib.fct_last_error()
+    # workspace queries are pure host arithmetic
+    assert lib.fct_sketch_workspace_bytes(1 << 20, 16, 256, 256) >= 256 * 16 * 8
+    assert lib.l1_sample_workspace_bytes(0) == 0
+    assert lib.fct_condition_workspace_bytes(64, 8) > 0
+    # bad s (not a power of two) with non-null dummies -> FCT_ERR_ARG before anything is enqueued
+    import ctypes
+    dummy = ctypes.c_void_p(16)
+    assert lib.fct_sketch(dummy, 10, 2, 2, dummy, dummy, dummy, 3, 4, dummy, 0, dummy, 1 << 20, None) == -1
+    assert lib.fct_sketch(dummy, 10, 2, 1, dummy, dummy, dummy, 4, 4, dummy, 0, dummy, 1 << 20, None) == -2
+    assert lib.l1_sample(dummy, 10, 0, 0, 1, dummy, dummy, 4, dummy, dummy, 1 << 20, None) == -1   # m < 1
+    assert lib.fct_condition(dummy, 4, 8, dummy, dummy, dummy, dummy, 1 << 20, None) == -2       # r1 < d

@@ -1,0 +1,270 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded inputs.
+
+Tolerances:
+  sketch   |Y_gpu - Y_oracle| <= 1e-5 * Mbound entrywise, Mbound = 4|B||C||H~||D||A| (north_star)
+  lambda   |lambda_gpu - lambda_oracle| <= 1e-5 * lambda_oracle per row, same Rinv and Pi2 (north_star)
+  sample   idx / weight bit-exact given identical p and uniforms (north_star)
+  R, Rinv  1e-9 relative to the matrix norm x cond, same fp32 Y (CholeskyQR2 vs Householder)
+"""
+import numpy as np
+import pytest
+
+import fctgen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+SK_TOL = 1e-5
+LAM_TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def fct():
+    import paper_1207_4684_b200 as m
+    from paper_1207_4684_b200 import build
+    build.build()
+    m.load()
+    return m
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def sketch_gpu(fct, inp, s=None, r1=None):
+    s = inp.s if s is None else s
+    r1 = inp.r1 if r1 is None else r1
+    Y = fct.fct_sketch(dev(inp.A), dev(inp.signs), dev(inp.cauchy), dev(inp.hash), s, r1)
+    return Y.cpu().numpy().astype(np.float64)
+
+
+def assert_sketch_close(Yg, Yo, Mb, tol=SK_TOL):
+    err = np.abs(Yg - Yo)
+    ratio = err / np.maximum(Mb, 1e-300)
+    worst = np.unravel_index(np.argmax(ratio), ratio.shape)
+    assert (err <= tol * Mb + 1e-30).all(), f"max err/Mbound = {ratio.max():.3e} at {worst}"
+
+
+# ---------------------------------------------------------------- K1 sketch
+@pytest.mark.parametrize("c", [1, 2, 3, 4, 5])
+def test_sketch_configs_ragged(fct, c):
+    """Each config's (d, s, r1, data kind) at a size spanning several blocks plus a ragged tail."""
+    cfg = fctgen.CONFIGS[c]
+    nblocks = {1: 40, 2: 20, 3: 9, 4: 6, 5: 3}[c]
+    n = nblocks * cfg.s + 37
+    inp = fctgen.make_inputs(cfg, n=n)
+    Yo, Mb = oracle.sketch(inp.A, inp.signs, inp.cauchy, inp.hash, cfg.s, cfg.r1)
+    Yg = sketch_gpu(fct, inp)
+    assert_sketch_close(Yg, Yo, Mb)
+
+
+@pytest.mark.parametrize("n,d,s,r1", [
+    (1, 1, 1, 1), (5, 3, 8, 2), (63, 7, 64, 16), (1000, 13, 16, 1), (1000, 33, 4, 128), (300, 1, 256, 64),
+    (4096, 130, 32, 8), (2048 + 5, 8, 2048, 64), (4096 + 1, 4, 4096, 32), (777, 5, 1, 4096), (2000, 40, 128, 20000),
+])
+def test_sketch_edge_shapes(fct, n, d, s, r1):
+    rng = np.random.default_rng(n * 31 + d)
+    n_pad = -(-n // s) * s
+    A = (rng.standard_normal((n, d)) * rng.choice([1e-3, 1.0, 1e3], (n, 1))).astype(np.float32)
+    sg = rng.choice(np.array([-1, 1], np.int8), n_pad)
+    c = rng.standard_cauchy(2 * n_pad).astype(np.float32)
+    h = rng.integers(0, r1, 2 * n_pad).astype(np.int32)
+    Yo, Mb = oracle.sketch(A, sg, c, h, s, r1)
+    Yg = fct.fct_sketch(dev(A), dev(sg), dev(c), dev(h), s, r1).cpu().numpy().astype(np.float64)
+    assert_sketch_close(Yg, Yo, Mb)
+
+
+def test_sketch_strided_accumulate_and_shards(fct):
+    """lda > d (a column slice of a wider matrix), accumulate=1, and s-aligned row shards."""
+    cfg = fctgen.CONFIGS[2]
+    inp = fctgen.make_inputs(cfg, n=8 * cfg.s)
+    wide = np.zeros((inp.A.shape[0], 24), np.float32)
+    wide[:, 3:3 + 16] = inp.A
+    Aw = dev(wide)[:, 3:3 + 16]
+    assert Aw.stride(0) == 24
+    sg, c, h = dev(inp.signs), dev(inp.cauchy), dev(inp.hash)
+    Yo, Mb = oracle.sketch(inp.A, inp.signs, inp.cauchy, inp.hash, cfg.s, cfg.r1)
+    Y = fct.fct_sketch(Aw, sg, c, h, cfg.s, cfg.r1)
+    assert_sketch_close(Y.cpu().numpy().astype(np.float64), Yo, Mb)
+    # shards with accumulate: Pi1 A = sum_g Pi1_g A_g
+    Ys = torch.zeros_like(Y)
+    for r0 in range(0, inp.A.shape[0], 3 * cfg.s):
+        r1_ = min(r0 + 3 * cfg.s, inp.A.shape[0])
+        fct.fct_sketch(Aw[r0:r1_], sg[r0:], c[2 * r0:], h[2 * r0:], cfg.s, cfg.r1, Y=Ys, accumulate=True)
+    assert_sketch_close(Ys.cpu().numpy().astype(np.float64), Yo, Mb)
+
+
+def test_sketch_errors(fct):
+    A = torch.zeros((10, 4), device="cuda")
+    sg = torch.ones(16, dtype=torch.int8, device="cuda")
+    c = torch.ones(32, device="cuda")
+    h = torch.full((32,), 99, dtype=torch.int32, device="cuda")
+    with pytest.raises(fct.FctError, match="FCT_ERR_ARG"):
+        fct.fct_sketch(A, sg, c, h, 3, 8)
+
+
+# ---------------------------------------------------------------- K5 conditioning
+@pytest.mark.parametrize("c", [1, 2, 3, 4, 5])
+def test_condition_matches_householder(fct, c):
+    cfg = fctgen.CONFIGS[c]
+    inp = fctgen.make_inputs(cfg, n=2 * cfg.s)
+    Y32 = oracle.sketch(inp.A, inp.signs, inp.cauchy, inp.hash, cfg.s, cfg.r1, with_bound=False).astype(np.float32)
+    R_o, Rinv_o, _ = oracle.condition(Y32.astype(np.float64))
+    R, Rinv, info = fct.fct_condition(dev(Y32))
+    R, Rinv = R.cpu().numpy(), Rinv.cpu().numpy()
+    cond = np.linalg.cond(Y32.astype(np.float64))
+    assert np.abs(R - R_o).max() <= 1e-12 * cond * np.abs(R_o).max()
+    assert np.abs(Rinv - Rinv_o).max() <= 1e-12 * cond * np.abs(Rinv_o).max()
+    assert (np.diag(R) > 0).all() and np.allclose(np.tril(R, -1), 0)
+
+
+def test_condition_singular_reports_info(fct):
+    Y = np.zeros((64, 4), np.float32)
+    Y[:, 0] = 1.0
+    Y[:, 1] = 1.0     # two equal columns -> rank deficient
+    with pytest.raises(fct.FctError, match="SINGULAR"):
+        fct.fct_condition(dev(Y))
+
+
+# ---------------------------------------------------------------- K2 row-norm
+def _rinv_for(inp):
+    """Rinv from the oracle's own conditioning of the oracle sketch (stage-wise parity input)."""
+    Y, _ = oracle.sketch(inp.A, inp.signs, inp.cauchy, inp.hash, inp.s, inp.r1)
+    R, Rinv, _ = oracle.condition(Y.astype(np.float32).astype(np.float64))
+    return Rinv
+
+
+@pytest.mark.parametrize("c", [1, 2, 3, 4, 5])
+def test_rownorm_configs(fct, c):
+    cfg = fctgen.CONFIGS[c]
+    inp = fctgen.make_inputs(cfg, n=2 * cfg.s)
+    Rinv = _rinv_for(inp)
+    # rows to score: a larger slice of the same matrix kind (ragged: not a multiple of 32)
+    B = fctgen.matrix(cfg.kind, cfg.seed, max(cfg.n, 20013), cfg.d, 0, 20000 + 13)
+    B[5] = 0.0
+    lam_o, tot_o = oracle.rownorm(B, Rinv, inp.pi2)
+    lam, tot = fct.l1_rownorm(dev(B), dev(Rinv), dev(inp.pi2))
+    lam = lam.cpu().numpy().astype(np.float64)
+    rel = np.abs(lam - lam_o) / np.maximum(lam_o, 1e-300)
+    assert lam[5] == 0.0
+    assert (np.abs(lam - lam_o) <= LAM_TOL * lam_o).all(), f"max rel {rel.max():.3e}"
+    np.testing.assert_allclose(float(tot.item()), lam.sum(), rtol=1e-12)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 7, 8, 16, 20, 27, 29, 32])
+def test_rownorm_all_k_and_identity(fct, k):
+    rng = np.random.default_rng(k)
+    d = 9
+    A = rng.standard_normal((1000, d)).astype(np.float32)
+    Rinv = np.triu(rng.standard_normal((d, d))) + 4 * np.eye(d)
+    Pi2 = rng.standard_cauchy((d, k)).astype(np.float32)
+    lam_o, _ = oracle.rownorm(A, Rinv, Pi2)
+    lam, _ = fct.l1_rownorm(dev(A), dev(Rinv), dev(Pi2))
+    lam = lam.cpu().numpy().astype(np.float64)
+    assert (np.abs(lam - lam_o) <= LAM_TOL * lam_o).all()
+    # identity: Rinv = I, Pi2 = I -> textbook median of |A| (many exact ties in the candidates)
+    I = np.eye(d, dtype=np.float32)
+    lam_i, _ = fct.l1_rownorm(dev(A), dev(np.eye(d)), dev(I))
+    np.testing.assert_allclose(lam_i.cpu().numpy(), np.median(np.abs(A.astype(np.float64)), axis=1),
+                               rtol=1e-7, atol=0)
+
+
+def test_probs_and_rownorm_probs(fct):
+    cfg = fctgen.CONFIGS[2]
+    inp = fctgen.make_inputs(cfg, n=4 * cfg.s)
+    Rinv = _rinv_for(inp)
+    lam_o, tot_o = oracle.rownorm(inp.A, Rinv, inp.pi2)
+    lam, p, tot = fct.l1_rownorm_probs(dev(inp.A), dev(Rinv), dev(inp.pi2))
+    lam = lam.cpu().numpy()
+    # p = (float)(lambda / total) from the GPU's own fp32 lambdas and fp64 total
+    want = (lam.astype(np.float64) / lam.astype(np.float64).sum()).astype(np.float32)
+    np.testing.assert_array_equal(p.cpu().numpy(), want)
+    np.testing.assert_allclose(float(tot.item()), tot_o, rtol=1e-6)
+
+
+# ---------------------------------------------------------------- K4 sampling (bit-exact)
+def _probs(n, seed, heavy=True):
+    rng = np.random.default_rng(seed)
+    lam = np.abs(rng.standard_cauchy(n)) if heavy else rng.random(n)
+    return (lam / lam.sum()).astype(np.float32)
+
+
+@pytest.mark.parametrize("n,m,row_base", [(1, 1, 0), (2047, 100, 0), (2049, 100, 7), (100000, 4096, 123456),
+                                          (1 << 20, 65536, 1 << 30)])
+def test_sample_bit_exact(fct, n, m, row_base):
+    p = _probs(n, n)
+    p[:3] = 1.0                                   # phat = 1 rows
+    idx, w, cnt = fct.l1_sample(dev(p), m, seed=99, row_base=row_base, capacity=2 * m + n // 10 + 64)
+    gi, gw, gc = fct.trim(idx, w, cnt)
+    oi, ow, oc = oracle.sample(p, m, seed=99, row_base=row_base)
+    assert gc == oc
+    np.testing.assert_array_equal(gi.numpy(), oi)
+    np.testing.assert_array_equal(gw.numpy(), ow)       # bitwise: 1/phat in IEEE fp64
+
+
+def test_sample_explicit_uniforms_and_capacity(fct):
+    n, m = 50000, 3000
+    p = _probs(n, 5, heavy=False)
+    u = fctgen.uniforms(17, 0, n)
+    idx, w, cnt = fct.l1_sample_u(dev(p), dev(u), m, capacity=100)
+    oi, ow, oc = oracle.sample(p, m, u=u)
+    c = int(cnt.item())
+    assert c == oc > 100                                  # count is exact even when it exceeds capacity
+    np.testing.assert_array_equal(idx.cpu().numpy()[:100], oi[:100])
+    np.testing.assert_array_equal(w.cpu().numpy()[:100], ow[:100])
+    # generator uniforms == the same uniforms passed explicitly
+    a = fct.trim(*fct.l1_sample(dev(p), m, seed=17, capacity=2 * m + 64))
+    b = fct.trim(*fct.l1_sample_u(dev(p), dev(u), m, capacity=2 * m + 64))
+    np.testing.assert_array_equal(a[0].numpy(), b[0].numpy())
+
+
+# ---------------------------------------------------------------- whole pipeline vs oracle pipeline
+@pytest.mark.parametrize("c", [1, 2])
+def test_pipeline_end_to_end(fct, c):
+    cfg = fctgen.CONFIGS[c]
+    n = min(cfg.n, 64 * cfg.s)
+    inp = fctgen.make_inputs(cfg, n=n)
+    P = fct.Pipeline(n, cfg.d, cfg.s, cfg.r1, cfg.k, cfg.m, seed=11)
+    P.run(dev(inp.A), dev(inp.signs), dev(inp.cauchy), dev(inp.hash), dev(inp.pi2))
+    torch.cuda.synchronize()
+    assert int(P.info.item()) == 0
+    Yo, Mb = oracle.sketch(inp.A, inp.signs, inp.cauchy, inp.hash, cfg.s, cfg.r1)
+    assert_sketch_close(P.Y.cpu().numpy().astype(np.float64), Yo, Mb)
+    _, Rinv_o, _ = oracle.condition(Yo)
+    lam_o, tot_o = oracle.rownorm(inp.A, Rinv_o, inp.pi2)
+    lam = P.lam.cpu().numpy().astype(np.float64)
+    # end-to-end (oracle's own R from its own fp64 Y): looser bound, DESIGN.md "Parity bar"
+    assert (np.abs(lam - lam_o) <= 1e-3 * lam_o + 1e-30).all()
+    p_o = oracle.probs(lam_o, tot_o)
+    oi, ow, oc = oracle.sample(p_o.astype(np.float32), cfg.m, seed=11)
+    gi, gw, gc = fct.trim(P.idx, P.weight, P.count)
+    # decisions may differ only where u is within the probability discrepancy of phat
+    u = fctgen.uniforms(11, 0, n)
+    phat = np.minimum(1.0, cfg.m * P.p.cpu().numpy().astype(np.float64))
+    diff = np.setxor1d(gi.numpy(), oi)
+    assert all(abs(u[i] - phat[i]) <= 2e-3 * phat[i] for i in diff)
+    # and the GPU's own decisions are exactly the Bernoulli rule on its p
+    oi2, ow2, _ = oracle.sample(P.p.cpu().numpy(), cfg.m, seed=11)
+    np.testing.assert_array_equal(gi.numpy(), oi2)
+    np.testing.assert_array_equal(gw.numpy(), ow2)
+
+
+def test_host_pipeline_matches_device_pipeline(fct):
+    cfg = fctgen.CONFIGS[2]
+    n = 32 * cfg.s
+    inp = fctgen.make_inputs(cfg, n=n)
+    H = fct.HostPipeline(n, cfg.d, cfg.s, cfg.r1, cfg.k, cfg.m, seed=5)
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+    hi, hw, hc = H.run(pin(inp.A), pin(inp.signs), pin(inp.cauchy), pin(inp.hash), pin(inp.pi2))
+    P = fct.Pipeline(n, cfg.d, cfg.s, cfg.r1, cfg.k, cfg.m, seed=5)
+    P.run(dev(inp.A), dev(inp.signs), dev(inp.cauchy), dev(inp.hash), dev(inp.pi2))
+    di, dw, dc = fct.trim(P.idx, P.weight, P.count)
+    # Y may differ bitwise between runs (shared-memory atomic order, reading R20), so p may
+    # differ by an ulp: same rows up to ambiguous ones, weights equal to fp32-ulp level
+    common, ih, idd = np.intersect1d(hi.numpy(), di.numpy(), return_indices=True)
+    assert len(common) >= 0.99 * max(hc, dc)
+    np.testing.assert_allclose(hw.numpy()[ih], dw.numpy()[idd], rtol=1e-6)
+    u = fctgen.uniforms(5, 0, n)
+    phat = np.minimum(1.0, cfg.m * P.p.cpu().numpy().astype(np.float64))
+    assert all(abs(u[i] - phat[i]) <= 1e-5 * phat[i] for i in np.setxor1d(hi.numpy(), di.numpy()))
