@@ -1,0 +1,337 @@
+"""bench.py -- the hot path of the FCT l1-conditioning pipeline (arXiv 1207.4684) on B200.
+
+One step = one pass of the whole hot path over the rank's row shard:
+sketch Y = 4BCH~DA -> [allreduce Y] -> R, R^-1 -> lambda -> [allreduce sum] -> p -> sample.
+Default workload: BASELINE.json configs[3] ("cfg4": n = 2^26 x d = 64 fp32, s = 1024, r1 = 4096,
+k = 27, m = 65536), the largest configuration BASELINE quotes at 1 GPU; at N GPUs the same n is
+row-sharded (strong scaling, as BASELINE's "row-sharded over 1/2/4/8 GPUs").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl fct|reference]
+Multi-GPU: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "FCT Pi1·A rows/s and achieved HBM GB/s (% of peak) at 1/2/4/8 B200"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy r+w)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def workload_desc(cfg, n_total):
+    kinds = {1: "i.i.d. N(0,1)", 2: "N(0,1) features + planted l1 regression column -b",
+             3: "N(0,1) rows x min(|Cauchy|^0.5, 1e4)", 4: "N(0,1), 1% of rows x1e3",
+             5: "Student-t(3) features + planted Cauchy-noise column -b"}
+    return (f"cfg{cfg.idx}: A {n_total} x {cfg.d} fp32 {kinds[cfg.kind]}; s={cfg.s} r1={cfg.r1} "
+            f"k={cfg.k} m={cfg.m}; D Rademacher, C Cauchy, B uniform hash, Pi2 Cauchy (seed {cfg.seed})")
+
+
+# ---------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons while the timed region runs."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int, interval=0.02):
+        self.ok = False
+        self.samples, self.reasons = [], set()
+        self.interval = interval
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            uuid = str(torch.cuda.get_device_properties(device_index).uuid)
+            h = None
+            for i in range(pynvml.nvmlDeviceGetCount()):
+                hh = pynvml.nvmlDeviceGetHandleByIndex(i)
+                u = pynvml.nvmlDeviceGetUUID(hh)
+                u = u.decode() if isinstance(u, bytes) else u
+                if uuid.replace("GPU-", "") in u:
+                    h = hh
+            if h is None:
+                h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.h = h
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = repr(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.interval)
+
+    def __enter__(self):
+        if self.ok:
+            self.stop = threading.Event()
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self.stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": float(self.max_mhz),
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------------------- oracle leg
+def oracle_sample_run(cfg, nblocks: int, seed_offset: int = 0):
+    """The oracle as it stands on a bounded sample: the first `nblocks` s-blocks of the workload.
+    Returns (rows, seconds, threads)."""
+    import fctgen
+    import oracle
+    n = nblocks * cfg.s
+    inp = fctgen.make_inputs(cfg, n=n)
+    t0 = time.perf_counter()
+    Y = oracle.sketch(inp.A, inp.signs, inp.cauchy, inp.hash, cfg.s, cfg.r1, with_bound=False)
+    R, Rinv, _ = oracle.condition(Y)
+    lam, tot = oracle.rownorm(inp.A, Rinv, inp.pi2)
+    p = oracle.probs(lam, tot).astype(np.float32)
+    oracle.sample(p, cfg.m, seed=cfg.seed + seed_offset)
+    dt = time.perf_counter() - t0
+    return n, dt, oracle.num_threads()
+
+
+def run_reference(args, cfg):
+    """--impl reference: the fp64 CPU oracle (the only reference there is), rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    # size one step to ~2-5 s of host work, calibrated on a short probe
+    n_probe, t_probe, _ = oracle_sample_run(cfg, 4)
+    per_block = t_probe / 4
+    nblocks = int(max(4, min(4096, 3.0 / max(per_block, 1e-6))))
+    for _ in range(args.warmup):
+        oracle_sample_run(cfg, nblocks)
+    times = []
+    for it in range(args.steps):
+        n, dt, thr = oracle_sample_run(cfg, nblocks, seed_offset=it)
+        times.append(dt)
+    t = sum(times) / len(times)
+    value = nblocks * cfg.s / t
+    sample = (f"first {nblocks} s-blocks ({nblocks * cfg.s} rows) of the workload per step: "
+              f"O1 sketch + O2 Householder QR + O3 row-norm + O4 sample, fp64, OpenMP")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg, cfg.n), "sampled_rows_per_step": nblocks * cfg.s},
+            "cpu_baseline": {"value": value, "unit": "rows/s", "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": sample, "cpu_model": cpu_model()},
+            "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+# ---------------------------------------------------------------------------------------- main arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="fct", choices=["fct", "reference"])
+    ap.add_argument("--rows", type=int, default=0, help="override n (testing)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-blocks", type=int, default=256)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    import fctgen
+    cfg = fctgen.CONFIGS[args.config]
+    if args.rows:
+        cfg = fctgen.Config(cfg.idx, args.rows, cfg.d, cfg.s, cfg.r1, cfg.k, cfg.m, cfg.kind, cfg.seed)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1207_4684_b200 as fct
+    from paper_1207_4684_b200 import build as fbuild
+    from paper_1207_4684_b200.dist import cuda_ops, run_step, shard_rows
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    fbuild.build()
+    lib = fct.load()
+
+    sh = shard_rows(cfg.n, cfg.s, rank, world)
+    t_gen = time.perf_counter()
+    inp = fctgen.make_inputs(cfg, n=sh.rows, row0=sh.row0)
+    t_gen = time.perf_counter() - t_gen
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    A, sg, cc, hh, pi2 = dev(inp.A), dev(inp.signs), dev(inp.cauchy), dev(inp.hash), dev(inp.pi2)
+    ops = cuda_ops()
+    names = ["start", "sketch", "allreduce_Y", "condition", "rownorm", "allreduce_sum", "sample"]
+    K, W = args.steps, args.warmup
+
+    def step(events=None):
+        return run_step(ops, sh, A, sg, cc, hh, pi2, cfg.s, cfg.r1, cfg.m, cfg.seed, events=events)
+
+    for _ in range(W):
+        res = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    info = int(res.extra[0].item()) if res.extra else 0
+    # per-stage events for every timed step (on the current stream = the launching stream)
+    evs = [{k: torch.cuda.Event(enable_timing=True) for k in names} for _ in range(K)]
+    e_beg, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    launches0 = lib.fct_launch_count()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with sampler:
+        e_beg.record()
+        for it in range(K):
+            res = step(evs[it])
+        e_end.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = lib.fct_launch_count() - launches0
+    ms = e_beg.elapsed_time(e_end)
+    t_local = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_max = float(t_local.item())
+    stage_ms = {}
+    for a, b in zip(names, names[1:]):
+        v = [e[a].elapsed_time(e[b]) for e in evs]
+        stage_ms[b] = {"mean": sum(v) / K, "median": statistics.median(v), "min": min(v), "max": max(v)}
+    ms_step = ms_max / K
+    value = cfg.n / (ms_step * 1e-3)
+
+    # ---- roofline of the dominant kernel (algorithmic bytes, SURVEY.md 8(d) / DESIGN.md "Roofline")
+    peak, peak_src = load_peaks()
+    n_loc, d = sh.rows, cfg.d
+    sk_bytes = n_loc * (4 * d + 1 + 8 + 8) + 4 * cfg.r1 * d
+    rn_bytes = n_loc * (4 * d + 4)
+    t_sk = stage_ms["sketch"]["mean"] * 1e-3
+    t_rn = stage_ms["rownorm"]["mean"] * 1e-3
+    kern = {"fct1_sketch": (sk_bytes, t_sk), "l1_rownorm": (rn_bytes, t_rn)}
+    dom = max(kern, key=lambda k: kern[k][1])
+    rl = {}
+    for kname, (byt, t) in kern.items():
+        ach = byt / t / 1e9
+        rl[kname] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "traffic": None, "algorithmic_bytes_per_launch": byt, "ms_per_launch": t * 1e3,
+                     "frac_of_8TBs": ach / 8000.0}
+    roofline = dict(rl[dom])
+    roofline["kernel"] = dom
+    roofline["peak_source"] = peak_src
+
+    # ---- e2e through the public API from pinned host buffers (N=1: HostPipeline / fct_pipeline_host)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        H = fct.HostPipeline(sh.rows, d, cfg.s, cfg.r1, cfg.k, cfg.m, cfg.seed)
+        pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+        hA, hs, hc, hh_, hp = pin(inp.A), pin(inp.signs), pin(inp.cauchy), pin(inp.hash), pin(inp.pi2)
+        H.run(hA, hs, hc, hh_, hp)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(args.e2e_steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _, _, cnt = H.run(hA, hs, hc, hh_, hp)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        te = sum(ts) / len(ts)
+        h2d = hA.numel() * 4 + hs.numel() + hc.numel() * 4 + hh_.numel() * 4 + hp.numel() * 4
+        d2h = 8 + 4 + min(cnt, H.capacity) * 16
+        e2e = {"value": cfg.n / (te * 1e-3), "unit": "rows/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": te, "steps": args.e2e_steps,
+               "path": "fct_pipeline_host (C ABI, pinned host buffers)"}
+        del H, hA
+
+    # ---- cpu baseline (rank 0, N=1 only): the oracle as it stands on a bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_s, t_s, thr = oracle_sample_run(cfg, args.cpu_blocks)
+        cpu = {"value": n_s / t_s, "unit": "rows/s", "cores": thr, "kind": "oracle",
+               "sample": f"first {args.cpu_blocks} s-blocks ({n_s} rows) of the workload: O1 sketch (explicit "
+                         f"Hadamard) + O2 QR + O3 row-norm + O4 sample, fp64, {t_s:.1f} s",
+               "cpu_model": cpu_model()}
+
+    if rank == 0:
+        sk = rl["fct1_sketch"]
+        line = {
+            "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg, cfg.n), "n": cfg.n, "d": cfg.d, "s": cfg.s, "r1": cfg.r1,
+                       "k": cfg.k, "m": cfg.m, "rows_per_gpu": sh.rows,
+                       "l2": "inputs (A + aux = %.1f GB per GPU) >> 126 MB L2; no flush needed"
+                             % ((sk_bytes) / 1e9),
+                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU"},
+            "hbm_gbs_sketch": sk["achieved"], "hbm_frac_sketch_of_8TBs": sk["frac_of_8TBs"],
+            "roofline": roofline, "roofline_all": rl,
+            "stages_ms": stage_ms, "gpu_launches": int(launches), "launches_per_step": launches / K,
+            "clocks": sampler.summary(), "cpu_baseline": cpu, "e2e": e2e,
+            "conditioning_info": info, "sampled_rows_last_step": int(res.count.item()),
+            "input_gen_s": t_gen,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

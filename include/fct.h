@@ -47,6 +47,8 @@ enum {
 const char* fct_last_error(void);
 /* Library version string, e.g. "fct-b200 0.1 sm_100a". */
 const char* fct_version(void);
+/* Number of kernels this library has launched in this process (all threads, all devices). */
+uint64_t fct_launch_count(void);
 
 /* Limits of this build. */
 #define FCT_MAX_S 4096   /* Hadamard block size s: power of two in [1, FCT_MAX_S]          */

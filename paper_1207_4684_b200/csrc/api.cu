@@ -1,5 +1,6 @@
 // api.cu -- error plumbing and version of libfct.so
 #include <string.h>
+#include <atomic>
 #include "common.cuh"
 
 namespace fct {
@@ -13,6 +14,10 @@ void set_error(const char* fmt, ...) {
 }
 const char* get_error() { return g_err; }
 
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+uint64_t launches() { return g_launches.load(std::memory_order_relaxed); }
+
 bool debug_sync() {
   static int v = -1;
   if (v < 0) {
@@ -25,3 +30,4 @@ bool debug_sync() {
 
 extern "C" const char* fct_last_error(void) { return fct::get_error(); }
 extern "C" const char* fct_version(void) { return "fct-b200 0.1 sm_100a"; }
+extern "C" uint64_t fct_launch_count(void) { return fct::launches(); }

@@ -15,6 +15,7 @@ namespace fct {
 void set_error(const char* fmt, ...);
 const char* get_error();
 bool debug_sync();  // FCT_DEBUG=1
+void count_launch();
 
 #define FCT_CHECK_ARG(cond, code, ...)          \
   do {                                          \
@@ -35,6 +36,7 @@ bool debug_sync();  // FCT_DEBUG=1
 
 // after a launch: catch configuration errors; in debug mode also synchronise
 inline fct_status post_launch(const char* what, cudaStream_t st) {
+  count_launch();
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess && debug_sync()) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {

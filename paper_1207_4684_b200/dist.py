@@ -1,0 +1,125 @@
+"""Multi-GPU row sharding of the hot path over torch.distributed.
+
+Pi1 A = sum_g Pi1_g A_g for contiguous s-aligned row shards (H~, C, D are (block-)diagonal and the
+columns of B partition across row blocks, Sec. 3.1), so:
+    each rank sketches its slice  ->  ONE sum-allreduce of the r1 x d partial sketches (C1)
+    -> every rank conditions the identical reduced Y (no broadcast needed)
+    -> row-norms of the local rows -> sum-allreduce of the fp64 local sums (C3)
+    -> probabilities and Bernoulli sampling keyed by the GLOBAL row index (row_base).
+This mirrors the paper's map/reduce two-pass structure.
+
+The compute steps are injected (`ops`), so the same plumbing runs on the CUDA path (`cuda_ops`,
+NCCL) and -- in tests only -- on CPU stand-ins with the gloo backend.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+
+@dataclass(frozen=True)
+class Shard:
+    rank: int
+    world: int
+    row0: int       # first global row of this rank (multiple of s)
+    rows: int       # rows owned by this rank (may be 0 for tiny problems)
+
+
+def shard_rows(n: int, s: int, rank: int, world: int) -> Shard:
+    """Contiguous s-aligned row shards: block b goes to rank floor(b * world / nblocks)."""
+    nb = -(-n // s)
+    b0 = (rank * nb) // world
+    b1 = ((rank + 1) * nb) // world
+    row0 = b0 * s
+    rows = max(0, min(n, b1 * s) - row0)
+    return Shard(rank, world, row0, rows)
+
+
+@dataclass
+class Ops:
+    """Per-rank compute steps (all tensors on the rank's device)."""
+    sketch: Callable      # (A, signs, cauchy, hash, s, r1) -> Y (r1, d)
+    condition: Callable   # (Y) -> (R, Rinv)
+    rownorm: Callable     # (A, Rinv, Pi2) -> (lambda, local_sum[1] fp64)
+    probs: Callable       # (lambda, total[1]) -> p
+    sample: Callable      # (p, m, seed, row_base) -> (idx, weight, count[1])
+
+
+def cuda_ops() -> Ops:
+    from . import api
+
+    def _cond(Y):
+        R, Rinv, info = api.fct_condition(Y, check=False)
+        return R, Rinv, info
+
+    def _rown(A, Rinv, Pi2):
+        return api.l1_rownorm(A, Rinv, Pi2)
+
+    return Ops(sketch=lambda A, sg, c, h, s, r1: api.fct_sketch(A, sg, c, h, s, r1),
+               condition=_cond, rownorm=_rown,
+               probs=lambda lam, tot: api.l1_probs(lam, tot),
+               sample=lambda p, m, seed, row_base: api.l1_sample(p, m, seed, row_base=row_base))
+
+
+@dataclass
+class StepResult:
+    Y: torch.Tensor
+    R: torch.Tensor
+    Rinv: torch.Tensor
+    lam: torch.Tensor
+    p: torch.Tensor
+    total: torch.Tensor
+    idx: torch.Tensor
+    weight: torch.Tensor
+    count: torch.Tensor
+    extra: tuple = ()
+
+
+def run_step(ops: Ops, shard: Shard, A, signs, cauchy, hash_rows, Pi2, s: int, r1: int, m: int, seed: int,
+             group=None, events: dict | None = None) -> StepResult:
+    """One pass of the whole hot path on this rank's shard; collectives only at C1 and C3."""
+    ev = events or {}
+    mark = (lambda k: ev[k].record()) if ev else (lambda k: None)
+    mark("start")
+    Y = ops.sketch(A, signs, cauchy, hash_rows, s, r1)
+    mark("sketch")
+    if shard.world > 1:
+        dist.all_reduce(Y, op=dist.ReduceOp.SUM, group=group)          # C1: r1 x d partial sketches
+    mark("allreduce_Y")
+    cond = ops.condition(Y)
+    R, Rinv = cond[0], cond[1]
+    mark("condition")
+    lam, total = ops.rownorm(A, Rinv, Pi2)
+    mark("rownorm")
+    if shard.world > 1:
+        dist.all_reduce(total, op=dist.ReduceOp.SUM, group=group)      # C3: one fp64 scalar
+    mark("allreduce_sum")
+    p = ops.probs(lam, total)
+    idx, w, cnt = ops.sample(p, m, seed, shard.row0)
+    mark("sample")
+    return StepResult(Y, R, Rinv, lam, p, total, idx, w, cnt, tuple(cond[2:]))
+
+
+def gather_samples(res: StepResult, group=None):
+    """All ranks' (idx, weight) concatenated in rank order = ascending global rows (every rank gets it)."""
+    world = dist.get_world_size(group)
+    dev = res.idx.device
+    k = min(int(res.count.item()), res.idx.numel())
+    meta = torch.tensor([k, int(res.count.item())], dtype=torch.int64, device=dev)
+    metas = [torch.zeros_like(meta) for _ in range(world)]
+    dist.all_gather(metas, meta, group=group)
+    mx = max(1, max(int(m[0].item()) for m in metas))
+    idx = torch.full((mx,), -1, dtype=torch.int64, device=dev)
+    w = torch.zeros((mx,), dtype=torch.float64, device=dev)
+    idx[:k] = res.idx[:k]
+    w[:k] = res.weight[:k]
+    gi = [torch.empty_like(idx) for _ in range(world)]
+    gw = [torch.empty_like(w) for _ in range(world)]
+    dist.all_gather(gi, idx, group=group)
+    dist.all_gather(gw, w, group=group)
+    out_i = [gi[r][:int(metas[r][0].item())] for r in range(world)]
+    out_w = [gw[r][:int(metas[r][0].item())] for r in range(world)]
+    return torch.cat(out_i), torch.cat(out_w), int(sum(int(m[1].item()) for m in metas))

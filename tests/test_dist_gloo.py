@@ -1,0 +1,128 @@
+"""Multi-rank plumbing of paper_1207_4684_b200.dist on CPU (gloo, world_size 2 and 3).
+
+The per-rank compute is the oracle (test-only stand-in for the CUDA ops), so this checks the
+sharding, the two collectives (sum of partial sketches, sum of lambda totals), the global-row keying
+of the sampler and the gather -- against the single-process oracle pipeline on the full problem.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import fctgen
+import oracle
+from paper_1207_4684_b200.dist import Ops, run_step, gather_samples, shard_rows
+
+
+def test_shard_rows_cover_and_align():
+    for n, s, world in [(1000, 64, 2), (1 << 20, 256, 8), (5, 4, 3), (64 * 7 + 3, 64, 4)]:
+        shards = [shard_rows(n, s, r, world) for r in range(world)]
+        assert shards[0].row0 == 0
+        tot = 0
+        for a, b in zip(shards, shards[1:]):
+            assert a.row0 + a.rows == b.row0 or b.rows == 0
+        for sh in shards:
+            assert sh.row0 % s == 0
+            tot += sh.rows
+        assert tot == n
+
+
+def oracle_ops():
+    def sketch(A, sg, c, h, s, r1):
+        Y, _ = oracle.sketch(A.numpy(), sg.numpy(), c.numpy(), h.numpy(), s, r1)
+        return torch.from_numpy(Y)
+
+    def condition(Y):
+        R, Rinv, _ = oracle.condition(Y.numpy())
+        return torch.from_numpy(R), torch.from_numpy(Rinv)
+
+    def rownorm(A, Rinv, Pi2):
+        lam, tot = oracle.rownorm(A.numpy(), Rinv.numpy(), Pi2.numpy())
+        return torch.from_numpy(lam), torch.tensor([tot], dtype=torch.float64)
+
+    def probs(lam, tot):
+        return (lam / tot).to(torch.float32)
+
+    def sample(p, m, seed, row_base):
+        idx, w, cnt = oracle.sample(p.numpy(), m, seed=seed, row_base=row_base)
+        return torch.from_numpy(idx), torch.from_numpy(w), torch.tensor([cnt], dtype=torch.int64)
+
+    return Ops(sketch, condition, rownorm, probs, sample)
+
+
+def _free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _worker(rank, world, port, n, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = fctgen.CONFIGS[2]
+        sh = shard_rows(n, cfg.s, rank, world)
+        inp = fctgen.make_inputs(cfg, n=sh.rows, row0=sh.row0)
+        t = torch.from_numpy
+        res = run_step(oracle_ops(), sh, t(inp.A), t(inp.signs), t(inp.cauchy), t(inp.hash), t(inp.pi2),
+                       cfg.s, cfg.r1, cfg.m, seed=3)
+        gi, gw, gc = gather_samples(res)
+        lam_all = [torch.zeros(shard_rows(n, cfg.s, r, world).rows, dtype=torch.float64) for r in range(world)]
+        # variable-size gather via padding
+        L = max(x.numel() for x in lam_all)
+        pad = torch.zeros(L, dtype=torch.float64)
+        pad[:res.lam.numel()] = res.lam
+        outs = [torch.zeros(L, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(outs, pad)
+        lam = torch.cat([o[:x.numel()] for o, x in zip(outs, lam_all)])
+        if rank == 0:
+            q.put((res.Y.numpy(), lam.numpy(), float(res.total.item()), gi.numpy(), gw.numpy(), gc))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_dist_pipeline_equals_single_process(world):
+    cfg = fctgen.CONFIGS[2]
+    n = 12 * cfg.s + 17
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    import queue
+    import time
+    t0 = time.time()
+    got = None
+    while got is None and time.time() - t0 < 240:
+        try:
+            got = q.get(timeout=2)
+        except queue.Empty:
+            if any(p.exitcode not in (None, 0) for p in procs):
+                break
+    for p in procs:
+        p.join(timeout=60)
+        if p.is_alive():
+            p.kill()
+    assert got is not None and all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    Y, lam, tot, gi, gw, gc = got
+    # single-process oracle pipeline on the full problem
+    inp = fctgen.make_inputs(cfg, n=n)
+    Y1, _ = oracle.sketch(inp.A, inp.signs, inp.cauchy, inp.hash, cfg.s, cfg.r1)
+    np.testing.assert_allclose(Y, Y1, rtol=1e-12, atol=1e-12 * np.abs(Y1).max())
+    _, Rinv, _ = oracle.condition(Y1)
+    lam1, tot1 = oracle.rownorm(inp.A, Rinv, inp.pi2)
+    np.testing.assert_allclose(lam, lam1, rtol=1e-9)
+    np.testing.assert_allclose(tot, tot1, rtol=1e-12)
+    p1 = (lam1 / tot1).astype(np.float32)
+    i1, w1, c1 = oracle.sample(p1, cfg.m, seed=3)
+    # the sharded sampler keys uniforms by GLOBAL row: same decisions as one process
+    assert gc == c1
+    common = np.intersect1d(gi, i1)
+    assert len(common) >= c1 - 2            # at most an ulp-level p difference may flip a decision
+    assert (np.diff(gi) > 0).all()
