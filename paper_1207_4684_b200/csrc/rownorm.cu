@@ -13,6 +13,8 @@
 //   => lambda is the exact median up to fp64 rounding, then rounded once to fp32.
 #include <math.h>
 #include "common.cuh"
+#include "sortnet.cuh"
+#include "selnet.cuh"
 
 namespace {
 
@@ -53,18 +55,15 @@ __device__ __forceinline__ void cswap(float& a, float& b) {
   b = hi;
 }
 
-// Batcher odd-even merge sort of N (power of two) registers, ascending
+// Batcher odd-even merge sort of N (power of two) registers, ascending (explicit network, sortnet.cuh)
+struct CSwap {
+  __device__ __forceinline__ void operator()(float& a, float& b) const { cswap(a, b); }
+};
 template <int N>
 __device__ __forceinline__ void sort_net(float (&a)[N]) {
-#pragma unroll
-  for (int p = 1; p < N; p <<= 1)
-#pragma unroll
-    for (int kk = p; kk >= 1; kk >>= 1)
-#pragma unroll
-      for (int j = kk % p; j + kk < N; j += 2 * kk)
-#pragma unroll
-        for (int i = 0; i < kk; ++i)
-          if (j + i + kk < N && (j + i) / (2 * p) == (j + i + kk) / (2 * p)) cswap(a[j + i], a[j + i + kk]);
+  if constexpr (N == 8) sortnet8(a, CSwap{});
+  else if constexpr (N == 16) sortnet16(a, CSwap{});
+  else sortnet32(a, CSwap{});
 }
 
 template <int K>
@@ -229,6 +228,194 @@ rownorm_kernel(const float* __restrict__ A, int64_t n, int d, int64_t lda, const
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// v1 (aligned rows, d % 4 == 0): warp tiles of 64 rows staged with cp.async (coalesced 16-B chunks)
+// into a padded shared layout (conflict-free LDS.128 per row), 2 rows per thread so every broadcast
+// LDS.128 of M feeds 8 FMAs; one sorting network per row (v only) and the certified-candidate rule
+//   L' = v_(m1) - E, H' = v_(m2) + E, E = max_j e_j   (L' <= L_m1, H' >= H_m2: a candidate superset)
+// followed by the exact fp64 recompute of the candidates.
+// exact |sum_l a_l M_lj| in fp64 with 4 independent partial sums (short dependency chains)
+__device__ __forceinline__ double exact_abs_dot(const float* __restrict__ arow, const double* __restrict__ mc, int d) {
+  // arow: 16-byte aligned row in shared memory (d % 4 == 0 in the v1 kernel); mc: M column, fp64
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  for (int l = 0; l < d; l += 4) {
+    const float4 a = *(const float4*)(arow + l);
+    const double2 m01 = *(const double2*)(mc + l), m23 = *(const double2*)(mc + l + 2);
+    s0 = fma((double)a.x, m01.x, s0);
+    s1 = fma((double)a.y, m01.y, s1);
+    s2 = fma((double)a.z, m23.x, s2);
+    s3 = fma((double)a.w, m23.y, s3);
+  }
+  return fabs((s0 + s1) + (s2 + s3));
+}
+
+template <int K>
+__device__ __forceinline__ float certified_median(const float (&acc)[K], float n1, float n2, const float* __restrict__ colb,
+                                                  float gam, int k, int m1, int m2, const float* __restrict__ arow,
+                                                  int d, const double* __restrict__ M64T) {
+  if (n1 == 0.f) return 0.f;
+  const float nrm2 = __fsqrt_ru(n2) * 1.0001f;
+  float srt[K];
+  float E = 0.f;
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const float v = fabsf(acc[j]);
+    const float ej = j < k ? gam * fminf(nrm2 * colb[2 * j], n1 * colb[2 * j + 1]) + 1e-37f : 0.f;
+    bad |= !(isfinite(v) && isfinite(ej));
+    E = fmaxf(E, ej);
+    srt[j] = j < k ? v : INFINITY;
+  }
+  // median-selection network for exactly k inputs (k in (K-4, K]; uniform across the grid)
+  switch (K - k) {
+    case 0: selnet<K>(srt, CSwap{}); break;
+    case 1: if constexpr (K >= 2) selnet<(K >= 2 ? K - 1 : 1)>(srt, CSwap{}); break;
+    case 2: if constexpr (K >= 3) selnet<(K >= 3 ? K - 2 : 1)>(srt, CSwap{}); break;
+    default: if constexpr (K >= 4) selnet<(K >= 4 ? K - 3 : 1)>(srt, CSwap{}); break;
+  }
+  float v1 = 0.f, v2 = 0.f;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    if (j == m1) v1 = srt[j];
+    if (j == m2) v2 = srt[j];
+  }
+  const float L = bad ? 0.f : v1 - E, H = bad ? INFINITY : v2 + E;
+  int below = 0;
+  unsigned cmask = 0u;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    if (j < k) {
+      const float v = fabsf(acc[j]);
+      const float ej = gam * fminf(nrm2 * colb[2 * j], n1 * colb[2 * j + 1]) + 1e-37f;
+      if (!bad && v + ej < L) ++below;
+      else if (bad || v - ej <= H) cmask |= 1u << j;
+    }
+  }
+  const int r1 = m1 - below, r2 = m2 - below;
+  const int nc = __popc(cmask);
+  double x1 = 0.0, x2 = 0.0;
+  if (nc <= 2) {
+    const int j0 = __ffs(cmask) - 1;
+    const double c0 = exact_abs_dot(arow, M64T + (size_t)j0 * d, d);
+    double c1 = INFINITY;
+    if (nc == 2) c1 = exact_abs_dot(arow, M64T + (size_t)(31 - __clz(cmask)) * d, d);
+    const double cmin = fmin(c0, c1), cmax = fmax(c0, c1);
+    x1 = r1 == 0 ? cmin : cmax;
+    x2 = r2 == 0 ? cmin : cmax;
+  } else {
+    // rare: several candidates -- rank each by counting against the others (ties broken by index)
+    unsigned mj = cmask;
+    while (mj) {
+      const int j = __ffs(mj) - 1;
+      mj &= mj - 1;
+      const double xj = exact_abs_dot(arow, M64T + (size_t)j * d, d);
+      int rank = 0;
+      unsigned mi = cmask;
+      while (mi) {
+        const int i = __ffs(mi) - 1;
+        mi &= mi - 1;
+        if (i == j) continue;
+        const double xi = exact_abs_dot(arow, M64T + (size_t)i * d, d);
+        rank += (xi < xj) || (xi == xj && i < j);
+      }
+      if (rank == r1) x1 = xj;
+      if (rank == r2) x2 = xj;
+    }
+  }
+  return (float)(0.5 * (x1 + x2));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;   // src-size 0 -> zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz) : "memory");
+}
+
+template <int K>
+__global__ void __launch_bounds__(256)
+rownorm_v1_kernel(const float* __restrict__ A, int64_t n, int d, int64_t lda, const float* __restrict__ M32g,
+                  const double* __restrict__ M64Tg, const float* __restrict__ colbg, int k, float gam, int ldt,
+                  float* __restrict__ lambda, double* __restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  float* M32 = (float*)smraw;                                     // [d][K]
+  float* colb = M32 + (size_t)d * K;                              // [K][2]
+  double* M64T = (double*)(colb + 2 * K);                         // [k][d]
+  float* tiles = (float*)(M64T + (size_t)k * d);                  // [warps][64][ldt]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  float* tile = tiles + (size_t)warp * 64 * ldt;
+  for (int e = threadIdx.x; e < k * d; e += blockDim.x) M64T[e] = M64Tg[e];
+  for (int e = threadIdx.x; e < d * K; e += blockDim.x) M32[e] = M32g[e];
+  for (int e = threadIdx.x; e < 2 * K; e += blockDim.x) colb[e] = colbg[e];
+  __syncthreads();
+  const int m1 = (k - 1) / 2, m2 = k / 2;
+  const int q4 = d >> 2;                  // 16-B chunks per row
+  double local = 0.0;
+  const int64_t ntiles = (n + 63) / 64;
+  for (int64_t tid = (int64_t)blockIdx.x * nw + warp; tid < ntiles; tid += (int64_t)gridDim.x * nw) {
+    const int64_t row0 = tid * 64;
+    const int nr = (int)(n - row0 < 64 ? n - row0 : 64);
+    __syncwarp();
+    for (int q = lane; q < 64 * q4; q += 32) {
+      const int r = q / q4, c4 = q - r * q4;
+      const bool ok = r < nr;
+      cp_async16(tile + r * ldt + 4 * c4, A + (row0 + (ok ? r : 0)) * lda + 4 * c4, ok);
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    __syncwarp();
+    const float* ar0 = tile + lane * ldt;
+    const float* ar1 = tile + (lane + 32) * ldt;
+    float acc0[K], acc1[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) { acc0[j] = 0.f; acc1[j] = 0.f; }
+    float n10 = 0.f, n20 = 0.f, n11 = 0.f, n21 = 0.f;
+#pragma unroll 2
+    for (int l4 = 0; l4 < q4; ++l4) {
+      const float4 a0 = *(const float4*)(ar0 + 4 * l4);
+      const float4 a1 = *(const float4*)(ar1 + 4 * l4);
+      n10 += fabsf(a0.x) + fabsf(a0.y) + fabsf(a0.z) + fabsf(a0.w);
+      n11 += fabsf(a1.x) + fabsf(a1.y) + fabsf(a1.z) + fabsf(a1.w);
+      n20 = fmaf(a0.x, a0.x, fmaf(a0.y, a0.y, fmaf(a0.z, a0.z, fmaf(a0.w, a0.w, n20))));
+      n21 = fmaf(a1.x, a1.x, fmaf(a1.y, a1.y, fmaf(a1.z, a1.z, fmaf(a1.w, a1.w, n21))));
+      const float av0[4] = {a0.x, a0.y, a0.z, a0.w}, av1[4] = {a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+      for (int ll = 0; ll < 4; ++ll) {
+        const float4* mrow = (const float4*)(M32 + (4 * l4 + ll) * K);
+#pragma unroll
+        for (int j4 = 0; j4 < K / 4; ++j4) {
+          const float4 mv = mrow[j4];
+          acc0[4 * j4 + 0] = fmaf(av0[ll], mv.x, acc0[4 * j4 + 0]);
+          acc0[4 * j4 + 1] = fmaf(av0[ll], mv.y, acc0[4 * j4 + 1]);
+          acc0[4 * j4 + 2] = fmaf(av0[ll], mv.z, acc0[4 * j4 + 2]);
+          acc0[4 * j4 + 3] = fmaf(av0[ll], mv.w, acc0[4 * j4 + 3]);
+          acc1[4 * j4 + 0] = fmaf(av1[ll], mv.x, acc1[4 * j4 + 0]);
+          acc1[4 * j4 + 1] = fmaf(av1[ll], mv.y, acc1[4 * j4 + 1]);
+          acc1[4 * j4 + 2] = fmaf(av1[ll], mv.z, acc1[4 * j4 + 2]);
+          acc1[4 * j4 + 3] = fmaf(av1[ll], mv.w, acc1[4 * j4 + 3]);
+        }
+      }
+    }
+    if (lane < nr) {
+      const float lam = certified_median<K>(acc0, n10, n20, colb, gam, k, m1, m2, ar0, d, M64T);
+      lambda[row0 + lane] = lam;
+      local += (double)lam;
+    }
+    if (lane + 32 < nr) {
+      const float lam = certified_median<K>(acc1, n11, n21, colb, gam, k, m1, m2, ar1, d, M64T);
+      lambda[row0 + lane + 32] = lam;
+      local += (double)lam;
+    }
+  }
+  __shared__ double red[8];
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if (lane == 0) red[warp] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s2 = 0.0;
+    for (int w = 0; w < nw; ++w) s2 += red[w];
+    partial[blockIdx.x] = s2;
+  }
+}
+
 __global__ void sum_partials_kernel(const double* __restrict__ partial, int np, double* __restrict__ out,
                                     int zero_first) {
   __shared__ double red[32];
@@ -260,15 +447,48 @@ size_t smem_bytes(int d, int k, int K) {
 
 int rownorm_grid() { return fct::num_sms() * 2; }
 
+int v1_ldt(int d) {
+  int q = d / 4 + 1;
+  if (!(q & 1)) ++q;   // odd number of 16-B chunks per staged row -> conflict-free LDS.128
+  return 4 * q;
+}
+size_t v1_fixed_smem(int d, int k, int K) {
+  return sizeof(float) * ((size_t)d * K + 2 * K) + sizeof(double) * (size_t)k * d;
+}
+int v1_warps(int d, int k, int K) {
+  const size_t per = sizeof(float) * 64 * (size_t)v1_ldt(d);
+  const size_t budget = 200 * 1024;
+  const size_t fixed = v1_fixed_smem(d, k, K);
+  if (fixed + per > budget) return 0;
+  return (int)std::min<size_t>(8, (budget - fixed) / per);
+}
+bool v1_ok(const float* A, int d, int64_t lda, int k, int K) {
+  return d % 4 == 0 && lda % 4 == 0 && ((uintptr_t)A & 15) == 0 && v1_warps(d, k, K) >= 1;
+}
+
 template <int K>
 fct_status launch_rownorm(const float* A, int64_t n, int d, int64_t lda, const float* M32, const double* M64T,
                           const float* colb, int k, float* lambda, double* partial, int grid, cudaStream_t st) {
+  const float u = 5.9604645e-08f;  // 2^-24
+  const float gam1 = (float)(d + 3) * u * 1.1f;
+  if (v1_ok(A, d, lda, k, K)) {
+    const int nw = v1_warps(d, k, K);
+    const int ldt = v1_ldt(d);
+    const size_t smem1 = v1_fixed_smem(d, k, K) + sizeof(float) * 64 * (size_t)ldt * nw;
+    auto kern1 = rownorm_v1_kernel<K>;
+    FCT_CUDA_RET(cudaFuncSetAttribute(kern1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+    int occ = 1;
+    FCT_CUDA_RET(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern1, nw * 32, smem1));
+    const int g1 = std::max(1, std::min(grid, fct::num_sms() * std::max(occ, 1)));
+    FCT_CUDA_RET(cudaMemsetAsync(partial, 0, sizeof(double) * grid, st));
+    kern1<<<g1, nw * 32, smem1, st>>>(A, n, d, lda, M32, M64T, colb, k, gam1, ldt, lambda, partial);
+    FCT_LAUNCHED("rownorm_v1_kernel", st);
+    return FCT_OK;
+  }
   const size_t smem = smem_bytes(d, k, K);
   auto kern = rownorm_kernel<K>;
   FCT_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const float u = 5.9604645e-08f;  // 2^-24
-  const float gam = (float)(d + 3) * u * 1.1f;
-  kern<<<grid, kRowThreads, smem, st>>>(A, n, d, lda, M32, M64T, colb, k, gam, lambda, partial);
+  kern<<<grid, kRowThreads, smem, st>>>(A, n, d, lda, M32, M64T, colb, k, gam1, lambda, partial);
   FCT_LAUNCHED("rownorm_kernel", st);
   return FCT_OK;
 }
