@@ -51,6 +51,34 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+
+// Batched shared-memory float add with ILP: all loads, then all CAS (ATOMS.CAS returns the old
+// word), then a retry loop for the (rare) lanes whose word changed in between.  Exact: an update is
+// applied only by a successful CAS on the value it read.
+template <int N>
+__device__ __forceinline__ void smem_add_batch(float* __restrict__ P, const int (&addr)[N], const float (&val)[N]) {
+  float old[N];
+#pragma unroll
+  for (int q = 0; q < N; ++q) old[q] = P[addr[q]];
+  unsigned pending = 0u;
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    const int want = __float_as_int(old[q]);
+    const int got = atomicCAS((int*)&P[addr[q]], want, __float_as_int(old[q] + val[q]));
+    if (got != want) pending |= 1u << q;
+  }
+  while (pending) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      if ((pending >> q) & 1u) {
+        const float o = P[addr[q]];
+        const int want = __float_as_int(o);
+        if (atomicCAS((int*)&P[addr[q]], want, __float_as_int(o + val[q])) == want) pending &= ~(1u << q);
+      }
+    }
+  }
+}
+
 template <int LA, int LB, int DT, int TILES_>
 struct Geo {
   static constexpr int S = 1 << (LA + LB);
@@ -142,11 +170,15 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
       for (int k0 = 0; k0 < RA; k0 += BA) {
         const int cur = (k0 / BA) & 1;
         if (k0 + BA < RA) load_a(cur ^ 1, k0 + BA);
+        int ad[BA];
+        float vv[BA];
 #pragma unroll
         for (int q = 0; q < BA; ++q) {
           x[k0 + q] *= (float)sgv[cur][q];
-          atomicAdd(&P[hv[cur][q] * DT + c], (4.f * cwv[cur][q]) * x[k0 + q]);
+          ad[q] = hv[cur][q] * DT + c;
+          vv[q] = (4.f * cwv[cur][q]) * x[k0 + q];
         }
+        smem_add_batch<BA>(P, ad, vv);
       }
 #pragma unroll
       for (int h = 1; h < RA; h <<= 1)
@@ -212,8 +244,14 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
                            hq[cur][1].x, hq[cur][1].y, hq[cur][1].z, hq[cur][1].w};
         const float cw[8] = {cq[cur][0].x, cq[cur][0].y, cq[cur][0].z, cq[cur][0].w,
                              cq[cur][1].x, cq[cur][1].y, cq[cur][1].z, cq[cur][1].w};
+        int ad[8];
+        float vv[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) atomicAdd(&P[hv[q] * DT + c], (sc * cw[q]) * y[gi][k0 + q]);
+        for (int q = 0; q < 8; ++q) {
+          ad[q] = hv[q] * DT + c;
+          vv[q] = (sc * cw[q]) * y[gi][k0 + q];
+        }
+        smem_add_batch<8>(P, ad, vv);
       }
     }
   }
