@@ -278,3 +278,17 @@ def test_sketch_generic_path_matches_too(fct, c, monkeypatch):
     inp = fctgen.make_inputs(cfg, n=5 * cfg.s + 3)
     Yo, Mb = oracle.sketch(inp.A, inp.signs, inp.cauchy, inp.hash, cfg.s, cfg.r1)
     assert_sketch_close(sketch_gpu(fct, inp), Yo, Mb)
+
+
+@pytest.mark.parametrize("c", [2, 4, 5])
+def test_rownorm_simt_path_matches_too(fct, c, monkeypatch):
+    """The SIMT row-norm kernel (fallback for unaligned / d > 128) stays parity-green."""
+    monkeypatch.setenv("FCT_ROWNORM_SIMT", "1")
+    cfg = fctgen.CONFIGS[c]
+    inp = fctgen.make_inputs(cfg, n=2 * cfg.s)
+    Rinv = _rinv_for(inp)
+    B = fctgen.matrix(cfg.kind, cfg.seed, max(cfg.n, 5000), cfg.d, 0, 5000 + 7)
+    lam_o, _ = oracle.rownorm(B, Rinv, inp.pi2)
+    lam, _ = fct.l1_rownorm(dev(B), dev(Rinv), dev(inp.pi2))
+    lam = lam.cpu().numpy().astype(np.float64)
+    assert (np.abs(lam - lam_o) <= LAM_TOL * lam_o).all()
