@@ -730,6 +730,293 @@ rownorm_tc_kernel(const __grid_constant__ CUtensorMap tmA, int64_t n, int d, con
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(tcols));
 }
 
+// ------------------------------------------------------------------------------------------------
+// ws: warp-specialised tcgen05 row-norm (one persistent CTA per SM, 16 warps).
+//   warps 0-3  ("split"): wait for the TMA'd tile, thread r <-> row r <-> TMEM lane r: norms -> smem,
+//              A_lo = A - trunc_tf32(A) -> TMEM; thread 0 issues the 3xTF32 MMAs into a rotating D buffer
+//              and the TMA loads (NA tile buffers ahead).
+//   warps 4-15 (3 epilogue groups of 4): group g takes tiles i = g (mod 3): tcgen05.ld D, certified
+//              median (candidates recomputed in fp64 from the row in global memory / L2), lambda.
+// All hand-offs are mbarriers; no CTA-wide barrier in the steady state.
+namespace wsk {
+constexpr int kSplitWarps = 4, kEpiGroups = 3, kThreads = 32 * (kSplitWarps + 4 * kEpiGroups);
+__device__ __forceinline__ void arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tc::su32(b)) : "memory");
+}
+__device__ __forceinline__ void wait(uint64_t* b, unsigned ph) {
+  asm volatile("{\n.reg .pred p;\nWW_%=:\nmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n@!p bra WW_%=;\n}\n"
+               ::"r"(tc::su32(b)), "r"(ph) : "memory");
+}
+__device__ __forceinline__ void init(uint64_t* b, unsigned cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc::su32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(tc::su32(b)) : "memory");
+}
+// exact |sum_l a_l M_lj| in fp64, row from global memory (16-byte aligned, d % 4 == 0)
+__device__ __forceinline__ double exact_abs_dot_g(const float* __restrict__ arow, const double* __restrict__ mc, int k,
+                                                  int d) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  for (int l = 0; l < d; l += 4) {
+    const float4 a = __ldg((const float4*)(arow + l));
+    s0 = fma((double)a.x, mc[(l + 0) * k], s0);
+    s1 = fma((double)a.y, mc[(l + 1) * k], s1);
+    s2 = fma((double)a.z, mc[(l + 2) * k], s2);
+    s3 = fma((double)a.w, mc[(l + 3) * k], s3);
+  }
+  return fabs((s0 + s1) + (s2 + s3));
+}
+}  // namespace wsk
+
+template <int K>
+__device__ __forceinline__ float certified_median_g(const float (&acc)[K], float n1, float n2,
+                                                    const float* __restrict__ colb, float gam, int k, int m1, int m2,
+                                                    const float* __restrict__ arow, int d,
+                                                    const double* __restrict__ M64) {
+  if (n1 == 0.f) return 0.f;
+  const float nrm2 = __fsqrt_ru(n2) * 1.0001f;
+  float srt[K], e[K];
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const float v = fabsf(acc[j]);
+    e[j] = j < k ? gam * fminf(nrm2 * colb[2 * j], n1 * colb[2 * j + 1]) + 1e-37f : 0.f;
+    bad |= !(isfinite(v) && isfinite(e[j]));
+    srt[j] = j < k ? v : INFINITY;
+  }
+  switch (K - k) {
+    case 0: selnet<K>(srt, CSwap{}); break;
+    case 1: if constexpr (K >= 2) selnet<(K >= 2 ? K - 1 : 1)>(srt, CSwap{}); break;
+    case 2: if constexpr (K >= 3) selnet<(K >= 3 ? K - 2 : 1)>(srt, CSwap{}); break;
+    default: if constexpr (K >= 4) selnet<(K >= 4 ? K - 3 : 1)>(srt, CSwap{}); break;
+  }
+  float v1 = 0.f, v2 = 0.f;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    if (j == m1) v1 = srt[j];
+    if (j == m2) v2 = srt[j];
+  }
+  float L = INFINITY, H = 0.f;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    if (j < k) {
+      const float v = fabsf(acc[j]);
+      if (v >= v1) L = fminf(L, v - e[j]);
+      if (v <= v2) H = fmaxf(H, v + e[j]);
+    }
+  }
+  if (bad) { L = 0.f; H = INFINITY; }
+  int below = 0;
+  unsigned cmask = 0u;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    if (j < k) {
+      const float v = fabsf(acc[j]);
+      if (!bad && v + e[j] < L) ++below;
+      else if (bad || v - e[j] <= H) cmask |= 1u << j;
+    }
+  }
+  const int r1 = m1 - below, r2 = m2 - below;
+  const int nc = __popc(cmask);
+  double x1 = 0.0, x2 = 0.0;
+  if (nc <= 2) {
+    const int j0 = __ffs(cmask) - 1;
+    const double c0 = wsk::exact_abs_dot_g(arow, M64 + j0, k, d);
+    double c1 = INFINITY;
+    if (nc == 2) c1 = wsk::exact_abs_dot_g(arow, M64 + (31 - __clz(cmask)), k, d);
+    const double cmin = fmin(c0, c1), cmax = fmax(c0, c1);
+    x1 = r1 == 0 ? cmin : cmax;
+    x2 = r2 == 0 ? cmin : cmax;
+  } else {
+    double ex[32];
+    int idx[32];
+    int m = 0;
+    unsigned mj = cmask;
+    while (mj) {
+      const int j = __ffs(mj) - 1;
+      mj &= mj - 1;
+      ex[m] = wsk::exact_abs_dot_g(arow, M64 + j, k, d);
+      idx[m++] = j;
+    }
+    for (int a = 0; a < m; ++a) {
+      int rank = 0;
+      for (int b = 0; b < m; ++b) rank += (ex[b] < ex[a]) || (ex[b] == ex[a] && idx[b] < idx[a]);
+      if (rank == r1) x1 = ex[a];
+      if (rank == r2) x2 = ex[a];
+    }
+  }
+  return (float)(0.5 * (x1 + x2));
+}
+
+template <int K>
+__global__ void __launch_bounds__(wsk::kThreads, 1)
+rownorm_ws_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ A, int64_t n, int d, int64_t lda,
+                  const float* __restrict__ M32g, const double* __restrict__ M64g, const float* __restrict__ colbg,
+                  int k, float gam, int NA, int ND, float* __restrict__ lambda, double* __restrict__ partial) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* base = smraw + ((1024u - (tc::su32(smraw) & 1023u)) & 1023u);
+  const int nch = (d + 31) >> 5;
+  const int KP = nch * 32;
+  const int tile_floats = nch * 128 * 32;
+  float* sA = (float*)base;                          // [NA][nch][128][32] (SW128)
+  float* sMhi = sA + NA * tile_floats;               // [nch][32][32] (SW128)
+  float* sMlo = sMhi + nch * 32 * 32;
+  double* M64 = (double*)(sMlo + nch * 32 * 32);     // [d][k]
+  float* colb = (float*)(M64 + (size_t)d * k);       // [K][2]
+  float* norms = colb + 2 * K;                       // [ND][128][2]
+  uint64_t* bars = (uint64_t*)(norms + (size_t)ND * 256 + 2);   // 8-aligned (offsets are multiples of 8 B)
+  uint64_t* tma_full = bars;                 // [NA]
+  uint64_t* a_free = tma_full + NA;          // [NA]   MMA done with the smem tile
+  uint64_t* alo_free = a_free + NA;          // [2]    MMA done with the TMEM A_lo buffer
+  uint64_t* d_full = alo_free + 2;           // [ND]   MMA result ready
+  uint64_t* n_full = d_full + ND;            // [ND]   norms written (128 arrivals)
+  uint64_t* d_free = n_full + ND;            // [ND]   epilogue done (4 arrivals)
+  __shared__ uint32_t tbase;
+  __shared__ double red[wsk::kThreads / 32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (tid == 0) {
+    for (int i = 0; i < NA; ++i) { wsk::init(&tma_full[i], 1); wsk::init(&a_free[i], 1); }
+    for (int i = 0; i < 2; ++i) wsk::init(&alo_free[i], 1);
+    for (int i = 0; i < ND; ++i) { wsk::init(&d_full[i], 1); wsk::init(&n_full[i], 128); wsk::init(&d_free[i], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tc::su32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int e = tid; e < 32 * KP; e += blockDim.x) {
+    const int j = e / KP, l = e - j * KP;
+    const float m = (j < K && l < d) ? M32g[l * K + j] : 0.f;
+    const float hi = tc::trunc_tf32(m), lo = m - hi;
+    const int off = (l >> 5) * 32 * 32 + j * 32 + ((((l & 31) >> 2) ^ (j & 7)) << 2) + (l & 3);
+    sMhi[off] = hi;
+    sMlo[off] = lo;
+  }
+  for (int e = tid; e < k * d; e += blockDim.x) M64[e] = M64g[e];
+  for (int e = tid; e < 2 * K; e += blockDim.x) colb[e] = colbg[e];
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase;
+  const uint32_t dcol0 = 2u * KP;   // D buffers after the two A_lo buffers
+  const int64_t ntiles = (n + 127) / 128;
+  const int64_t t0 = blockIdx.x, tstep = gridDim.x;
+  const int64_t my_tiles = t0 < ntiles ? (ntiles - 1 - t0) / tstep + 1 : 0;
+  double local = 0.0;
+
+  if (warp < wsk::kSplitWarps) {
+    // ------------------------------------------------------------------ split + MMA issue + TMA
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(32 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const int ksteps = (d + 7) >> 3;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    if (tid == 0)
+      for (int64_t i = 0; i < my_tiles && i < NA; ++i)
+        tc::tma_tile(sA + (i % NA) * tile_floats, &tmA, nch, (int)((t0 + i * tstep) * 128), &tma_full[i % NA]);
+    for (int64_t i = 0; i < my_tiles; ++i) {
+      const int sa = (int)(i % NA), sd = (int)(i % ND), sl = (int)(i & 1);
+      wsk::wait(&tma_full[sa], (unsigned)((i / NA) & 1));
+      if (i >= 2) wsk::wait(&alo_free[sl], (unsigned)(((i - 2) >> 1) & 1));
+      if (i >= ND) wsk::wait(&d_free[sd], (unsigned)(((i - ND) / ND) & 1));
+      const float* tile = sA + sa * tile_floats;
+      float s1 = 0.f, s2 = 0.f;
+      for (int q = 0; q < nch; ++q) {
+        uint32_t lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 v = *(const float4*)(tile + q * 128 * 32 + tid * 32 + ((c ^ (tid & 7)) << 2));
+          const float a[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            s1 += fabsf(a[w]);
+            s2 = fmaf(a[w], a[w], s2);
+            lo[c * 4 + w] = __float_as_uint(a[w] - tc::trunc_tf32(a[w]));
+          }
+        }
+        tc::st32(tm + lane_off + (uint32_t)(sl * KP + q * 32), lo);
+      }
+      norms[(sd * 128 + tid) * 2] = s1;
+      norms[(sd * 128 + tid) * 2 + 1] = s2;
+      wsk::arrive(&n_full[sd]);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (tid == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t tD = tm + dcol0 + (uint32_t)(sd * 32);
+        int cnt = 0;
+        for (int pass = 0; pass < 3; ++pass) {
+          const float* Bm = pass == 1 ? sMlo : sMhi;
+          for (int ks = 0; ks < ksteps; ++ks) {
+            const int q = ks >> 2, kin = ks & 3;
+            const uint64_t bd = tc::sdesc((const unsigned char*)(Bm + q * 32 * 32) + kin * 32);
+            const uint32_t accf = cnt > 0 ? 1u : 0u;
+            if (pass < 2) {
+              const uint64_t ad = tc::sdesc((const unsigned char*)(tile + q * 128 * 32) + kin * 32);
+              asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+                           ::"r"(tD), "l"(ad), "l"(bd), "r"(idesc), "r"(accf));
+            } else {
+              const uint32_t ta = tm + (uint32_t)(sl * KP + ks * 8);
+              asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n"
+                           ::"r"(tD), "r"(ta), "l"(bd), "r"(idesc), "r"(accf));
+            }
+            ++cnt;
+          }
+        }
+        wsk::commit(&d_full[sd]);
+        wsk::commit(&alo_free[sl]);
+        wsk::commit(&a_free[sa]);
+        // refill the tile buffer of the previous tile once its MMA is done
+        if (i >= 1 && i - 1 + NA < my_tiles) {
+          const int pa = (int)((i - 1) % NA);
+          wsk::wait(&a_free[pa], (unsigned)(((i - 1) / NA) & 1));
+          tc::tma_tile(sA + pa * tile_floats, &tmA, nch, (int)((t0 + (i - 1 + NA) * tstep) * 128), &tma_full[pa]);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue groups
+    const int ew = warp - wsk::kSplitWarps;
+    const int g = ew >> 2, qd = ew & 3;
+    const int m1 = (k - 1) / 2, m2 = k / 2;
+    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+    for (int64_t i = g; i < my_tiles; i += wsk::kEpiGroups) {
+      const int sd = (int)(i % ND);
+      const unsigned ph = (unsigned)((i / ND) & 1);
+      wsk::wait(&d_full[sd], ph);
+      wsk::wait(&n_full[sd], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t dv[32];
+      tc::ld32(tm + lane_off + dcol0 + (uint32_t)(sd * 32), dv);
+      const int r = qd * 32 + lane;
+      const float n1 = norms[(sd * 128 + r) * 2], n2 = norms[(sd * 128 + r) * 2 + 1];
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) wsk::arrive(&d_free[sd]);   // D and the norms are in registers
+      float acc[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc[j] = __uint_as_float(dv[j]);
+      const int64_t row = (t0 + i * tstep) * 128 + r;
+      if (row < n) {
+        const float lam = certified_median_g<K>(acc, n1, n2, colb, gam, k, m1, m2, A + row * lda, d, M64);
+        lambda[row] = lam;
+        local += (double)lam;
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if (lane == 0) red[warp] = local;
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < wsk::kThreads / 32; ++w) s += red[w];
+    partial[blockIdx.x] = s;
+  }
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+
 __global__ void sum_partials_kernel(const double* __restrict__ partial, int np, double* __restrict__ out,
                                     int zero_first) {
   __shared__ double red[32];
@@ -836,8 +1123,44 @@ fct_status launch_tc(const float* A, int64_t n, int d, int64_t lda, const float*
 }
 
 template <int K>
+fct_status launch_ws(const float* A, int64_t n, int d, int64_t lda, const float* M32, const double* M64,
+                     const float* colb, int k, float* lambda, double* partial, int grid, cudaStream_t st) {
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)n};
+  cuuint64_t strides[1] = {(cuuint64_t)lda * sizeof(float)};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t es[2] = {1, 1};
+  CUresult cr = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)A, dims, strides, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  FCT_CHECK_ARG(cr == CUDA_SUCCESS, FCT_ERR_CUDA, "l1_rownorm: cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  const int nch = (d + 31) / 32, KP = nch * 32;
+  const int ND = (512 - 2 * KP) / 32;               // D buffers in TMEM after two A_lo buffers
+  const size_t fixed = 1024 + sizeof(float) * (2 * (size_t)nch * 32 * 32) + sizeof(double) * (size_t)k * d +
+                       sizeof(float) * (2 * K + (size_t)ND * 256 + 2) + sizeof(uint64_t) * (3 * (size_t)ND + 2 + 2 * 4);
+  const size_t tileb = sizeof(float) * (size_t)nch * 128 * 32;
+  const size_t budget = 232448 - 2048;
+  int NA = (int)std::min<size_t>(4, (budget - fixed) / tileb);
+  if (NA < 2 || ND < 4) return FCT_ERR_UNSUPPORTED;
+  const size_t smem = fixed + tileb * NA;
+  auto kern = rownorm_ws_kernel<K>;
+  FCT_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int g = std::max(1, std::min(grid, fct::num_sms()));
+  if (fct::debug_sync()) fprintf(stderr, "[fct] rownorm_ws: grid %d NA %d ND %d smem %zu\n", g, NA, ND, smem);
+  const float gam = 6.103515625e-05f * 1.05f;   // 3xTF32 bound (see rownorm_tc_kernel)
+  FCT_CUDA_RET(cudaMemsetAsync(partial, 0, sizeof(double) * grid, st));
+  kern<<<g, wsk::kThreads, smem, st>>>(map, A, n, d, lda, M32, M64, colb, k, gam, NA, ND, lambda, partial);
+  FCT_LAUNCHED("rownorm_ws_kernel", st);
+  return FCT_OK;
+}
+
+template <int K>
 fct_status launch_rownorm(const float* A, int64_t n, int d, int64_t lda, const float* M32, const double* M64,
                           const float* colb, int k, float* lambda, double* partial, int grid, cudaStream_t st) {
+  if (tc_ok(A, n, d, lda) && !getenv("FCT_ROWNORM_TC1")) {
+    const fct_status r = launch_ws<K>(A, n, d, lda, M32, M64, colb, k, lambda, partial, grid, st);
+    if (r != FCT_ERR_UNSUPPORTED) return r;
+  }
   if (tc_ok(A, n, d, lda)) return launch_tc<K>(A, n, d, lda, M32, M64, colb, k, lambda, partial, grid, st);
   const float u = 5.9604645e-08f;  // 2^-24
   const float gam1 = (float)(d + 3) * u * 1.1f;

@@ -101,17 +101,68 @@ __device__ __forceinline__ int swz(int r) {
   return G > 1 ? (r ^ ((r >> LB) & (G - 1))) : r;
 }
 
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// packed fp32x2 add / sub (FADD2 on sm_100)
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long r, x = *(unsigned long long*)&a, y = *(unsigned long long*)&b;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+  return *(float2*)&r;
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  unsigned long long r, x = *(unsigned long long*)&a, y = *(unsigned long long*)&b;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+  return *(float2*)&r;
+}
+// in-register unnormalised Walsh-Hadamard transform of R values (natural order): stage 1 scalar,
+// stages 2..R/2 on packed pairs (two independent butterflies per FADD2)
+template <int R>
+__device__ __forceinline__ void fwht_regs(float (&x)[R]) {
+#pragma unroll
+  for (int k = 0; k < R; k += 2) {
+    const float a = x[k], b = x[k + 1];
+    x[k] = a + b;
+    x[k + 1] = a - b;
+  }
+#pragma unroll
+  for (int h = 2; h < R; h <<= 1)
+#pragma unroll
+    for (int k = 0; k < R; k += 2)
+      if (!(k & h)) {
+        const float2 a = make_float2(x[k], x[k + 1]), b = make_float2(x[k + h], x[k + h + 1]);
+        const float2 s2 = add2(a, b), d2 = sub2(a, b);
+        x[k] = s2.x; x[k + 1] = s2.y;
+        x[k + h] = d2.x; x[k + h + 1] = d2.y;
+      }
+}
+
+// aux bytes staged per block: identity half = signs[S] (padded to 16) + cauchy[S] + hash[S];
+// Hadamard half = cauchy[S] + hash[S]
+template <int S>
+struct AuxLayout {
+  static constexpr int sign_bytes = (S + 15) / 16 * 16;
+  static constexpr int id_bytes = sign_bytes + 8 * S;
+  static constexpr int had_bytes = 8 * S;
+};
+
 template <int LA, int LB, int DT, int TL>
 __global__ void __launch_bounds__(Geo<LA, LB, DT, TL>::THREADS, 1)
 sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, const int8_t* __restrict__ signs,
                  const float* __restrict__ cauchy, const int32_t* __restrict__ hash, int r1, int nslices,
                  int64_t nblocks, float inv_sqrt_s, double* __restrict__ W) {
   using Gm = Geo<LA, LB, DT, TL>;
+  using AL = AuxLayout<Gm::S>;
   constexpr int S = Gm::S, RA = Gm::RA, RB = Gm::RB, NT = Gm::NT, NB = Gm::NB, TILES = Gm::TILES, G = Gm::G;
   extern __shared__ __align__(128) unsigned char smraw[];
-  float* tiles = (float*)smraw;                                     // [TILES][S][DT]
-  float* P = (float*)(smraw + TILES * Gm::tile_bytes);             // [r1][DT]
-  __shared__ __align__(8) uint64_t bars[TILES];
+  // [TILES] tiles | [TILES] identity aux | [TILES] Hadamard aux | P[r1][DT]
+  float* tiles = (float*)smraw;
+  unsigned char* auxI0 = smraw + TILES * Gm::tile_bytes;
+  unsigned char* auxH0 = auxI0 + TILES * AL::id_bytes;
+  float* P = (float*)(auxH0 + TILES * AL::had_bytes);
+  __shared__ __align__(8) uint64_t bar_t[TILES], bar_i[TILES], bar_h[TILES];
 
   const int cs = blockIdx.x % nslices;
   const int grp = blockIdx.x / nslices;
@@ -121,75 +172,93 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
   const int lt = threadIdx.x - tg * NT;   // thread within the tile group
   const int c = lt % DT;
   float* tile = tiles + (size_t)tg * S * DT;
-  uint64_t* bar = &bars[tg];
+  unsigned char* auxI = auxI0 + tg * AL::id_bytes;
+  unsigned char* auxH = auxH0 + tg * AL::had_bytes;
+  const int8_t* sSign = (const int8_t*)auxI;
+  const float* sCi = (const float*)(auxI + AL::sign_bytes);
+  const int* sHi = (const int*)(auxI + AL::sign_bytes + 4 * S);
+  const float* sCh = (const float*)auxH;
+  const int* sHh = (const int*)(auxH + 4 * S);
 
   for (int e = threadIdx.x; e < r1 * DT; e += blockDim.x) P[e] = 0.f;
-  if (threadIdx.x < TILES) mbar_init(&bars[threadIdx.x], 1);
+  if (threadIdx.x < TILES) {
+    mbar_init(&bar_t[threadIdx.x], 1);
+    mbar_init(&bar_i[threadIdx.x], 1);
+    mbar_init(&bar_h[threadIdx.x], 1);
+  }
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncthreads();
+
+  auto issue_tile = [&](int64_t bb) {
+    mbar_expect_tx(&bar_t[tg], (unsigned)Gm::tile_bytes);
+#pragma unroll
+    for (int q = 0; q < S / Gm::BOXR; ++q)
+      tma_load_2d(tile + (size_t)q * Gm::BOXR * DT, &tmap, c0, (int)(bb * S + q * Gm::BOXR), &bar_t[tg]);
+  };
+  // signs: bulk-copy the 16-byte-aligned prefix of the block's valid rows; the (rare) tail past it is
+  // read from global memory in phase A
+  auto sign_bulk = [&](int64_t bb) -> int {
+    const int64_t valid = n - bb * S < S ? n - bb * S : S;
+    return (int)(valid & ~15LL);
+  };
+  auto issue_id = [&](int64_t bb) {
+    const int sb = sign_bulk(bb);
+    const int64_t t0 = 2 * bb * S;
+    mbar_expect_tx(&bar_i[tg], (unsigned)(sb + 8 * S));
+    if (sb > 0) bulk_g2s(auxI, signs + bb * S, (unsigned)sb, &bar_i[tg]);
+    bulk_g2s(auxI + AL::sign_bytes, cauchy + t0 + S, 4u * S, &bar_i[tg]);
+    bulk_g2s(auxI + AL::sign_bytes + 4 * S, hash + t0 + S, 4u * S, &bar_i[tg]);
+  };
+  auto issue_had = [&](int64_t bb) {
+    const int64_t t0 = 2 * bb * S;
+    mbar_expect_tx(&bar_h[tg], 8u * S);
+    bulk_g2s(auxH, cauchy + t0, 4u * S, &bar_h[tg]);
+    bulk_g2s(auxH + 4 * S, hash + t0, 4u * S, &bar_h[tg]);
+  };
 
   // blocks of this tile group: b = grp + ngrp * (tg + TILES * t)
   const int64_t bstep = (int64_t)ngrp * TILES;
   int64_t b = grp + (int64_t)ngrp * tg;
   if (lt == 0 && b < nblocks) {
-    mbar_expect_tx(bar, (unsigned)Gm::tile_bytes);
-#pragma unroll
-    for (int q = 0; q < S / Gm::BOXR; ++q)
-      tma_load_2d(tile + (size_t)q * Gm::BOXR * DT, &tmap, c0, (int)(b * S + q * Gm::BOXR), bar);
+    issue_tile(b);
+    issue_id(b);
+    issue_had(b);
   }
   unsigned phase = 0;
+  const float sc_h = 4.f * inv_sqrt_s;
   for (; b < nblocks; b += bstep) {
-    mbar_wait(bar, phase);
-    phase ^= 1u;
+    const int64_t bn = b + bstep;
+    mbar_wait(&bar_t[tg], phase);
+    mbar_wait(&bar_i[tg], phase);
     const int64_t rowb = b * S;
-    const int64_t t0 = 2 * rowb;  // first H~-row of the block
-    // ---------------- phase A: rows g + (S/RA) k
+    const int sb = sign_bulk(b);
+    // ---------------- phase A: rows g + (S/RA) k; identity half scattered from the staged aux
     {
       const int g = lt / DT;
       float x[RA];
 #pragma unroll
       for (int k = 0; k < RA; ++k) x[k] = tile[(g + (S / RA) * k) * DT + c];
-      // aux loads software-pipelined one batch ahead of the shared-memory atomics (which would
-      // otherwise serialise them behind the CAS loops)
       constexpr int BA = RA < 8 ? RA : 8;
-      int sgv[2][BA], hv[2][BA];
-      float cwv[2][BA];
-      auto load_a = [&](int buf, int k0) {
-#pragma unroll
-        for (int q = 0; q < BA; ++q) {
-          const int r = g + (S / RA) * (k0 + q);
-          const int64_t row = rowb + r;
-          const int64_t t = t0 + S + r;
-          sgv[buf][q] = row < n ? (int)__ldg(signs + row) : 0;   // converted at use, not at load
-          cwv[buf][q] = __ldg(cauchy + t);
-          hv[buf][q] = __ldg(hash + t);
-        }
-      };
-      load_a(0, 0);
 #pragma unroll
       for (int k0 = 0; k0 < RA; k0 += BA) {
-        const int cur = (k0 / BA) & 1;
-        if (k0 + BA < RA) load_a(cur ^ 1, k0 + BA);
         int ad[BA];
         float vv[BA];
 #pragma unroll
         for (int q = 0; q < BA; ++q) {
-          x[k0 + q] *= (float)sgv[cur][q];
-          ad[q] = hv[cur][q] * DT + c;
-          vv[q] = (4.f * cwv[cur][q]) * x[k0 + q];
+          const int r = g + (S / RA) * (k0 + q);
+          int sg;
+          if (r < sb) sg = sSign[r];
+          else sg = rowb + r < n ? (int)__ldg(signs + rowb + r) : 0;
+          x[k0 + q] *= (float)sg;
+          ad[q] = sHi[r] * DT + c;
+          vv[q] = (4.f * sCi[r]) * x[k0 + q];
         }
         smem_add_batch<BA>(P, ad, vv);
       }
-#pragma unroll
-      for (int h = 1; h < RA; h <<= 1)
-#pragma unroll
-        for (int k = 0; k < RA; ++k)
-          if (!(k & h)) {
-            const float a = x[k], bb = x[k + h];
-            x[k] = a + bb;
-            x[k + h] = a - bb;
-          }
-      named_bar(1 + tg, NT);  // everyone has read the TMA tile
+      fwht_regs<RA>(x);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      named_bar(1 + tg, NT);  // everyone has read the TMA tile and the identity aux
+      if (lt == 0 && bn < nblocks) issue_id(bn);
 #pragma unroll
       for (int k = 0; k < RA; ++k) tile[swz<LB, G>(g + (S / RA) * k) * DT + c] = x[k];
     }
@@ -203,57 +272,35 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
       for (int k = 0; k < RB; ++k) y[gi][k] = tile[swz<LB, G>(RB * gp + k) * DT + c];
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    named_bar(1 + tg, NT);  // the buffer is free: prefetch the next block
-    const int64_t bn = b + bstep;
-    if (lt == 0 && bn < nblocks) {
-      mbar_expect_tx(bar, (unsigned)Gm::tile_bytes);
-#pragma unroll
-      for (int q = 0; q < S / Gm::BOXR; ++q)
-        tma_load_2d(tile + (size_t)q * Gm::BOXR * DT, &tmap, c0, (int)(bn * S + q * Gm::BOXR), bar);
-    }
+    named_bar(1 + tg, NT);  // the tile buffer is free: prefetch the next block
+    if (lt == 0 && bn < nblocks) issue_tile(bn);
+    mbar_wait(&bar_h[tg], phase);
+    phase ^= 1u;
 #pragma unroll
     for (int gi = 0; gi < NB; ++gi) {
       const int gp = lt / DT + (NT / DT) * gi;
-#pragma unroll
-      for (int h = 1; h < RB; h <<= 1)
-#pragma unroll
-        for (int k = 0; k < RB; ++k)
-          if (!(k & h)) {
-            const float a = y[gi][k], bb = y[gi][k + h];
-            y[gi][k] = a + bb;
-            y[gi][k + h] = a - bb;
-          }
-      // contiguous rows: 16-byte vector loads of (hash, cauchy), 8 rows per batch, one batch ahead
-      const int64_t tb = t0 + RB * gp;
+      fwht_regs<RB>(y[gi]);
       static_assert(RB % 8 == 0, "phase B batches");
-      int4 hq[2][2];
-      float4 cq[2][2];
-      auto load_b = [&](int buf, int k0) {
-        hq[buf][0] = __ldg((const int4*)(hash + tb + k0));
-        hq[buf][1] = __ldg((const int4*)(hash + tb + k0 + 4));
-        cq[buf][0] = __ldg((const float4*)(cauchy + tb + k0));
-        cq[buf][1] = __ldg((const float4*)(cauchy + tb + k0 + 4));
-      };
-      load_b(0, 0);
-      const float sc = 4.f * inv_sqrt_s;
 #pragma unroll
       for (int k0 = 0; k0 < RB; k0 += 8) {
-        const int cur = (k0 / 8) & 1;
-        if (k0 + 8 < RB) load_b(cur ^ 1, k0 + 8);
-        const int hv[8] = {hq[cur][0].x, hq[cur][0].y, hq[cur][0].z, hq[cur][0].w,
-                           hq[cur][1].x, hq[cur][1].y, hq[cur][1].z, hq[cur][1].w};
-        const float cw[8] = {cq[cur][0].x, cq[cur][0].y, cq[cur][0].z, cq[cur][0].w,
-                             cq[cur][1].x, cq[cur][1].y, cq[cur][1].z, cq[cur][1].w};
+        const int r0 = RB * gp + k0;
+        const int4 h0 = *(const int4*)(sHh + r0), h1 = *(const int4*)(sHh + r0 + 4);
+        const float4 q0 = *(const float4*)(sCh + r0), q1 = *(const float4*)(sCh + r0 + 4);
+        const int hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        const float cw[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
         int ad[8];
         float vv[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           ad[q] = hv[q] * DT + c;
-          vv[q] = (sc * cw[q]) * y[gi][k0 + q];
+          vv[q] = (sc_h * cw[q]) * y[gi][k0 + q];
         }
         smem_add_batch<8>(P, ad, vv);
       }
     }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    named_bar(1 + tg, NT);  // the Hadamard aux is free
+    if (lt == 0 && bn < nblocks) issue_had(bn);
   }
   __syncthreads();
   for (int e = threadIdx.x; e < r1 * DT; e += blockDim.x) {
@@ -292,7 +339,8 @@ fct_status launch_v1(const float* A, int64_t n, int64_t d, int64_t lda, const in
   FCT_CHECK_ARG(cr == CUDA_SUCCESS, FCT_ERR_CUDA, "fct_sketch: cuTensorMapEncodeTiled failed (%d)", (int)cr);
   const int nslices = (int)((d + DT - 1) / DT);
   const int64_t nblocks = (n + s - 1) / s;
-  const size_t smem = Gm::TILES * Gm::tile_bytes + (size_t)r1 * DT * sizeof(float);
+  const size_t smem = Gm::TILES * (Gm::tile_bytes + AuxLayout<Gm::S>::id_bytes + AuxLayout<Gm::S>::had_bytes) +
+                      (size_t)r1 * DT * sizeof(float);
   auto kern = sketch_v1_kernel<LA, LB, DT, TL>;
   FCT_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 1;
@@ -310,12 +358,13 @@ fct_status launch_v1(const float* A, int64_t n, int64_t d, int64_t lda, const in
   return FCT_OK;
 }
 
-constexpr size_t kV1Smem = 220 * 1024;
+constexpr size_t kV1Smem = 232448 - 256;   // max dynamic shared memory per block on sm_100, less static
 
 template <int LA, int LB, int DT, int TL>
 bool fits(int r1) {
   using Gm = Geo<LA, LB, DT, TL>;
-  return Gm::TILES * Gm::tile_bytes + (size_t)r1 * DT * sizeof(float) <= kV1Smem;
+  return Gm::TILES * (Gm::tile_bytes + AuxLayout<Gm::S>::id_bytes + AuxLayout<Gm::S>::had_bytes) +
+             (size_t)r1 * DT * sizeof(float) <= kV1Smem;
 }
 
 }  // namespace
@@ -323,7 +372,8 @@ bool fits(int r1) {
 // Returns FCT_ERR_UNSUPPORTED (without enqueueing) when no v1 instance covers (s, d, r1, alignment).
 fct_status fct_sketch_v1(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs, const float* cauchy,
                          const int32_t* hash, int s, int r1, double* W, cudaStream_t st) {
-  if (((uintptr_t)A & 15) || ((uintptr_t)cauchy & 15) || ((uintptr_t)hash & 15) || (lda % 4) || n >= (1LL << 31))
+  if (((uintptr_t)A & 15) || ((uintptr_t)cauchy & 15) || ((uintptr_t)hash & 15) || ((uintptr_t)signs & 15) ||
+      (lda % 4) || n >= (1LL << 31))
     return FCT_ERR_UNSUPPORTED;
 #define TRY(LA_, LB_, DT_, TL_)                                                              \
   if (s == (1 << (LA_ + LB_)) && fits<LA_, LB_, DT_, TL_>(r1) && (DT_ <= 8 || d >= DT_))     \
