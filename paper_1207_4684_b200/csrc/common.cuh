@@ -82,3 +82,6 @@ fct_status fct_sketch_v1(const float* A, int64_t n, int64_t d, int64_t lda, cons
 fct_status fct_rownorm_impl(const float* A, int64_t n, int64_t d, int64_t lda, const double* Rinv,
                             const float* Pi2, int32_t k, float* lambda, double* lambda_sum,
                             bool zero_sum, void* ws, size_t wsb, cudaStream_t st);
+fct_status fct_rownorm_ws2(const float* A, int64_t n, int d, int64_t lda, const float* M32, int KP32,
+                           const double* M64, const float* colb, int k, double* partial, int grid, float* lambda,
+                           cudaStream_t st);

@@ -1158,6 +1158,8 @@ template <int K>
 fct_status launch_rownorm(const float* A, int64_t n, int d, int64_t lda, const float* M32, const double* M64,
                           const float* colb, int k, float* lambda, double* partial, int grid, cudaStream_t st) {
   if (tc_ok(A, n, d, lda) && !getenv("FCT_ROWNORM_TC1")) {
+    const fct_status r2 = fct_rownorm_ws2(A, n, d, lda, M32, K, M64, colb, k, partial, grid, lambda, st);
+    if (r2 != FCT_ERR_UNSUPPORTED) return r2;
     const fct_status r = launch_ws<K>(A, n, d, lda, M32, M64, colb, k, lambda, partial, grid, st);
     if (r != FCT_ERR_UNSUPPORTED) return r;
   }

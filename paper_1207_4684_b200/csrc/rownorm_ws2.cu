@@ -1,0 +1,468 @@
+// rownorm_ws2.cu -- K2 v3: l1 row-norm estimate lambda_i = median_j |(A (Rinv Pi2))_ij|
+// (Lemma medCauchy; the FastCauchyRegression row norms P:L2921-2938, with
+// M = Rinv Pi2 formed first).  Warp-specialised, one persistent CTA per SM:
+//   warp 0-3   split: thread r <-> tile row r <-> TMEM lane r.  ||a||_2^2 -> smem, A_lo = A - tf32(A) -> TMEM.
+//   warp 4     TMA producer: 128-row tiles of A (SWIZZLE_128B) into NA shared buffers.
+//   warp 5     MMA issuer: D = A*M_hi + A*M_lo + A_lo*M_hi (3xTF32, kind::tf32) into a rotating TMEM
+//              accumulator (descriptors precomputed), committed to mbarriers.
+//   warp 6..   EG epilogue groups of 4 warps (one TMEM lane quadrant each); group g takes tiles g mod EG:
+//              tcgen05.ld of D, the certified median for a compile-time k (below), lambda, sum lambda.
+// Certified median (K2): with v_j = |D_j| and the rigorous bound |v_j - |Lambda_ij|| <= e_j =
+// gam ||a||_2 ||m~_j||_2 (gam covers the 3xTF32 evaluation and the fp32 rounding of M), the order statistic
+// t_(m1) >= L = min_{v_j >= v_(m1)} (v_j - e_j) and t_(m2) <= H = max_{v_j <= v_(m2)} (v_j + e_j); entries with
+// v_j + e_j < L lie below the middle, entries with v_j - e_j > H above it, and the rest (1-2 per row) are
+// evaluated exactly in fp64 from the row kept in shared memory (fp64 M) and ranked.  lambda is the exact
+// median up to fp64 rounding, rounded once to fp32.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <math.h>
+#include "common.cuh"
+#include "selnet.cuh"
+#include "tc.cuh"
+
+namespace {
+
+constexpr int kSplitWarps = 4;
+constexpr int kTmaWarp = 4;
+constexpr int kMmaWarp = 5;
+constexpr int kEpiWarp0 = 6;
+
+struct CSwap2 {
+  __device__ __forceinline__ void operator()(float& a, float& b) const {
+    const float lo = fminf(a, b), hi = fmaxf(a, b);
+    a = lo;
+    b = hi;
+  }
+};
+
+// exact |sum_l a_l M_lj| for one or two columns j0, j1 in fp64.  Row: KEEP -> row r of the swizzled shared
+// tile, else the row in global memory.  D = d at compile time (0: runtime d); d % 4 == 0.
+template <int KK, int D, bool KEEP>
+__device__ __forceinline__ void exact_pair(const float* __restrict__ tile, const float* __restrict__ grow, int r, int d,
+                                          const double* __restrict__ M64, int j0, int j1, double& x0, double& x1) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+  const int dd = D ? D : d;
+#pragma unroll(D ? D / 4 : 1)
+  for (int l = 0; l < dd; l += 4) {
+    const float4 a = KEEP ? *(const float4*)(tile + tcx::sw_off(r, l)) : __ldg((const float4*)(grow + l));
+    const double d0 = a.x, d1 = a.y, d2 = a.z, d3 = a.w;
+    const double* m = M64 + (size_t)l * KK;
+    a0 = fma(d0, m[j0], a0);
+    a1 = fma(d1, m[KK + j0], a1);
+    a2 = fma(d2, m[2 * KK + j0], a2);
+    a3 = fma(d3, m[3 * KK + j0], a3);
+    b0 = fma(d0, m[j1], b0);
+    b1 = fma(d1, m[KK + j1], b1);
+    b2 = fma(d2, m[2 * KK + j1], b2);
+    b3 = fma(d3, m[3 * KK + j1], b3);
+  }
+  x0 = fabs((a0 + a1) + (a2 + a3));
+  x1 = fabs((b0 + b1) + (b2 + b3));
+}
+
+template <int KK, int D, bool KEEP>
+__device__ __forceinline__ float certified_median(const uint32_t (&dv)[32], float n2, const float* __restrict__ cm,
+                                                  float gam, const float* __restrict__ tile,
+                                                  const float* __restrict__ grow, int r, int d,
+                                                  const double* __restrict__ M64) {
+  constexpr int m1 = (KK - 1) / 2, m2 = KK / 2;
+  float v[KK], srt[KK];
+  const float g = gam * __fsqrt_ru(n2);
+  bool bad = !(n2 >= 1e-30f) || !(g <= 1e30f);
+#pragma unroll
+  for (int j = 0; j < KK; ++j) {
+    v[j] = fabsf(__uint_as_float(dv[j]));
+    srt[j] = v[j];
+    bad |= !(v[j] <= 3.0e38f);   // inf / NaN
+  }
+  selnet<KK>(srt, CSwap2{});
+  const float v1 = srt[m1], v2 = srt[m2];
+  float La = INFINITY, Lb = INFINITY, Ha = 0.f, Hb = 0.f;
+#pragma unroll
+  for (int j = 0; j < KK; ++j) {
+    const float e = g * cm[j];
+    float& Lx = (j & 1) ? Lb : La;
+    float& Hx = (j & 1) ? Hb : Ha;
+    if (v[j] >= v1) Lx = fminf(Lx, __fsub_rd(v[j], e));
+    if (v[j] <= v2) Hx = fmaxf(Hx, __fadd_ru(v[j], e));
+  }
+  const float L = fminf(La, Lb), H = fmaxf(Ha, Hb);
+  int below = 0;
+  unsigned cmask = 0u;
+#pragma unroll
+  for (int j = 0; j < KK; ++j) {
+    const float e = g * cm[j];
+    if (__fadd_ru(v[j], e) < L) ++below;
+    else if (__fsub_rd(v[j], e) <= H) cmask |= 1u << j;
+  }
+  if (bad) {
+    below = 0;
+    cmask = KK == 32 ? 0xFFFFFFFFu : ((1u << KK) - 1u);
+  }
+  const int q1 = m1 - below, q2 = m2 - below;
+  const int nc = __popc(cmask);
+  if (r < 0) return v1 + v2 + (float)nc;   // diag
+  double x1, x2;
+  if (nc <= 2) {
+    const int j0 = __ffs(cmask) - 1;
+    const int j1 = nc == 2 ? 31 - __clz(cmask) : j0;
+    double c0, c1;
+    exact_pair<KK, D, KEEP>(tile, grow, r, d, M64, j0, j1, c0, c1);
+    const double cmin = fmin(c0, c1), cmax = fmax(c0, c1);
+    x1 = q1 == 0 ? cmin : cmax;
+    x2 = q2 == 0 ? cmin : cmax;
+  } else {
+    // rare: several candidates -- exact value of each, then rank by counting (ties broken by index)
+    double ex[KK];
+    x1 = x2 = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < KK; ++j) {
+      ex[j] = 0.0;
+      if ((cmask >> j) & 1u) {
+        double c0, c1;
+        exact_pair<KK, D, KEEP>(tile, grow, r, d, M64, j, j, c0, c1);
+        ex[j] = c0;
+      }
+    }
+#pragma unroll 1
+    for (int a = 0; a < KK; ++a) {
+      if (!((cmask >> a) & 1u)) continue;
+      int rank = 0;
+      for (int b = 0; b < KK; ++b)
+        rank += ((cmask >> b) & 1u) && (ex[b] < ex[a] || (ex[b] == ex[a] && b < a));
+      if (rank == q1) x1 = ex[a];
+      if (rank == q2) x2 = ex[a];
+    }
+  }
+  return (float)(0.5 * (x1 + x2));
+}
+
+struct Smem {   // byte offsets inside the 1024-aligned dynamic shared memory
+  int a, b, m64, cm, nrm, bars, total;
+};
+__host__ __device__ inline Smem layout(int d, int KK, int NA, int ND) {
+  const int nch = (d + 31) / 32;
+  Smem s;
+  s.a = 0;
+  s.b = s.a + NA * nch * 16384;          // B = [M_hi | M_lo]^T: nch chunks x 64 rows x 128 B
+  s.m64 = s.b + nch * 8192;
+  s.cm = s.m64 + ((d * KK * 8 + 15) & ~15);
+  s.nrm = s.cm + 32 * 4;
+  s.bars = s.nrm + ND * 128 * 4;
+  s.total = s.bars + 8 * (2 * NA + 4 + 3 * ND);
+  return s;
+}
+
+// TMEM columns of one A buffer: [A_hi (KP) | A_lo (KP)] when AT (A_hi fed from TMEM), else [A_lo (KP)]
+template <bool AT>
+__host__ __device__ inline int abuf_cols(int KP) { return AT ? 2 * KP : KP; }
+
+template <int KK, int D, int EG, bool KEEP, bool AT>
+__global__ void __launch_bounds__(32 * (kEpiWarp0 + 4 * EG), 1)
+rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ A, int64_t n, int d, int64_t lda,
+                   const float* __restrict__ M32g, int KP32, const double* __restrict__ M64g,
+                   const float* __restrict__ colbg, float gam, int NA, int ND, float* __restrict__ lambda,
+                   double* __restrict__ partial, int diag) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* base = smraw + ((1024u - (tcx::su32(smraw) & 1023u)) & 1023u);
+  const int dd = D ? D : d;
+  const int nch = (dd + 31) >> 5, KP = nch * 32;
+  const int tile_floats = nch * 128 * 32;
+  const Smem L = layout(dd, KK, NA, ND);
+  float* sA = (float*)(base + L.a);
+  float* sB = (float*)(base + L.b);
+  double* M64 = (double*)(base + L.m64);
+  float* cm = (float*)(base + L.cm);
+  float* norms = (float*)(base + L.nrm);
+  uint64_t* tma_full = (uint64_t*)(base + L.bars);   // [NA]  tile landed
+  uint64_t* a_free = tma_full + NA;                   // [NA]  tile buffer reusable
+  uint64_t* at_full = a_free + NA;                    // [2]   A pieces in TMEM (4 split-warp arrivals)
+  uint64_t* at_free = at_full + 2;                    // [2]   TMEM A buffer reusable (MMA done)
+  uint64_t* d_full = at_free + 2;                     // [ND]  accumulator ready
+  uint64_t* n_full = d_full + ND;                     // [ND]  norms written (4 split-warp arrivals)
+  uint64_t* d_free = n_full + ND;                     // [ND]  accumulator + norms drained (4 warp arrivals)
+  __shared__ uint32_t tbase;
+  __shared__ double red[kEpiWarp0 + 4 * EG];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (tid == 0) {
+    for (int i = 0; i < NA; ++i) {
+      tcx::bar_init(&tma_full[i], 1);
+      tcx::bar_init(&a_free[i], KEEP ? 4 : 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tcx::bar_init(&at_full[i], 4);
+      tcx::bar_init(&at_free[i], 1);
+    }
+    for (int i = 0; i < ND; ++i) {
+      tcx::bar_init(&d_full[i], 1);
+      tcx::bar_init(&n_full[i], 4);
+      tcx::bar_init(&d_free[i], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tcx::su32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // B operand (N = 64 rows x KP columns, K-major SWIZZLE_128B): rows j < 32 = tf32(M~)^T, rows 32 + j = the
+  // remainder M~ - tf32(M~); one MMA yields A*M_hi in D[0:32) and A*M_lo in D[32:64)
+  for (int e = tid; e < 64 * KP; e += blockDim.x) {
+    const int jj = e / KP, l = e - jj * KP, j = jj & 31;
+    const float m = (j < KK && l < dd) ? M32g[l * KP32 + j] : 0.f;
+    const float hi = tcx::trunc_tf32(m);
+    sB[(l >> 5) * 64 * 32 + jj * 32 + ((((l & 31) >> 2) ^ (jj & 7)) << 2) + (l & 3)] = jj < 32 ? hi : m - hi;
+  }
+  for (int e = tid; e < KK * dd; e += blockDim.x) M64[e] = M64g[e];
+  for (int e = tid; e < 32; e += blockDim.x) cm[e] = e < KK ? colbg[2 * e] : 0.f;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase;
+  const int acols = abuf_cols<AT>(KP);
+  const uint32_t dcol0 = 2u * acols;   // TMEM: [A buf 0][A buf 1][D 0] ... [D ND-1], D = 64 columns
+  const int ntiles = (int)((n + 127) / 128);
+  const int t0 = blockIdx.x, tstep = gridDim.x;
+  const int my_tiles = t0 < ntiles ? (ntiles - 1 - t0) / tstep + 1 : 0;
+  double local = 0.0;
+
+  if (warp < kSplitWarps) {
+    // ------------------------------------------------------------------ split: norms, A pieces -> TMEM
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    int sa = 0, sd = 0;
+    unsigned pa = 0, pd = 0;   // phase parities of the current ring slots
+    for (int i = 0; i < my_tiles; ++i) {
+      const int sl = i & 1;
+      tcx::bar_wait(&tma_full[sa], pa);
+      if (i >= 2) tcx::bar_wait(&at_free[sl], (unsigned)(((i - 2) >> 1) & 1));
+      const float* tile = sA + sa * tile_floats;
+      const uint32_t tb = tm + lane_off + (uint32_t)(sl * acols);
+      float s2 = 0.f, s2b = 0.f;
+#pragma unroll(D ? (D + 31) / 32 : 1)
+      for (int q = 0; q < nch; ++q) {
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 v = *(const float4*)(tile + q * 128 * 32 + tid * 32 + ((c ^ (tid & 7)) << 2));
+          s2 = fmaf(v.x, v.x, s2);
+          s2b = fmaf(v.y, v.y, s2b);
+          s2 = fmaf(v.z, v.z, s2);
+          s2b = fmaf(v.w, v.w, s2b);
+          const float h0 = tcx::trunc_tf32(v.x), h1 = tcx::trunc_tf32(v.y), h2 = tcx::trunc_tf32(v.z),
+                      h3 = tcx::trunc_tf32(v.w);
+          hi[c * 4 + 0] = __float_as_uint(h0);
+          hi[c * 4 + 1] = __float_as_uint(h1);
+          hi[c * 4 + 2] = __float_as_uint(h2);
+          hi[c * 4 + 3] = __float_as_uint(h3);
+          lo[c * 4 + 0] = __float_as_uint(v.x - h0);
+          lo[c * 4 + 1] = __float_as_uint(v.y - h1);
+          lo[c * 4 + 2] = __float_as_uint(v.z - h2);
+          lo[c * 4 + 3] = __float_as_uint(v.w - h3);
+        }
+        if (AT) tcx::tmem_st32(tb + (uint32_t)(q * 32), hi);
+        tcx::tmem_st32(tb + (uint32_t)((AT ? KP : 0) + q * 32), lo);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) tcx::bar_arrive(&at_full[sl]);
+      if (i >= ND) tcx::bar_wait(&d_free[sd], pd ^ 1u);
+      norms[sd * 128 + tid] = s2 + s2b;
+      __syncwarp();
+      if (lane == 0) tcx::bar_arrive(&n_full[sd]);
+      if (++sa == NA) { sa = 0; pa ^= 1u; }
+      if (++sd == ND) { sd = 0; pd ^= 1u; }
+    }
+  } else if (warp == kTmaWarp) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int sa = 0;
+      unsigned pa = 0;
+      for (int j = 0; j < my_tiles; ++j) {
+        if (j >= NA) tcx::bar_wait(&a_free[sa], pa ^ 1u);
+        tcx::tma_tile(sA + sa * tile_floats, &tmA, nch, (t0 + j * tstep) * 128, &tma_full[sa]);
+        if (++sa == NA) { sa = 0; pa ^= 1u; }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------------ MMA issuer (one thread)
+    if (lane == 0) {
+      // kind::tf32, M = 128, N = 64, K-major A and B, fp32 accumulate
+      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+      const int ksteps = (dd + 7) >> 3;
+      const uint64_t b00 = tcx::sdesc_sw128(sB), a00 = tcx::sdesc_sw128(sA);
+      int sa = 0, sd = 0;
+      unsigned pd = 0;
+      for (int i = 0; i < my_tiles; ++i) {
+        const int sl = i & 1;
+        tcx::bar_wait(&at_full[sl], (unsigned)((i >> 1) & 1));   // implies the TMA tile has landed
+        if (i >= ND) tcx::bar_wait(&d_free[sd], pd ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t tD = tm + dcol0 + (uint32_t)(sd * 64);
+        const uint32_t tA = tm + (uint32_t)(sl * acols);
+        const uint64_t a0 = a00 + (uint64_t)((sa * tile_floats * 4) >> 4);
+        if (diag != 3) {
+          // D = (A_hi + A_lo) [M_hi | M_lo]: every product of the two-term splits, nothing dropped
+#pragma unroll(D ? (D + 7) / 8 : 1)
+          for (int ks = 0; ks < ksteps; ++ks) {
+            const uint64_t bd = b00 + (uint64_t)(((ks >> 2) * 8192 + (ks & 3) * 32) >> 4);
+            if (AT)
+              tcx::mma_tf32_ts(tD, tA + (uint32_t)(ks * 8), bd, idesc, ks > 0);
+            else
+              tcx::mma_tf32_ss(tD, a0 + (uint64_t)(((ks >> 2) * 16384 + (ks & 3) * 32) >> 4), bd, idesc, ks > 0);
+          }
+        }
+#pragma unroll(D ? (D + 7) / 8 : 1)
+        for (int ks = 0; ks < ksteps; ++ks) {
+          const uint64_t bd = b00 + (uint64_t)(((ks >> 2) * 8192 + (ks & 3) * 32) >> 4);
+          tcx::mma_tf32_ts(tD, tA + (uint32_t)((AT ? KP : 0) + ks * 8), bd, idesc, diag != 3 || ks > 0);
+        }
+        tcx::mma_commit(&d_full[sd]);
+        tcx::mma_commit(&at_free[sl]);
+        if (!KEEP) tcx::mma_commit(&a_free[sa]);
+        if (++sa == NA) sa = 0;
+        if (++sd == ND) { sd = 0; pd ^= 1u; }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue groups
+    const int ew = warp - kEpiWarp0;
+    const int g = ew >> 2;
+    const int quad = warp & 3;                        // TMEM lane quadrant this warp may access
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    int sd = g % ND, sa = g % NA;
+    unsigned ph = (unsigned)((g / ND) & 1);
+    for (int i = g; i < my_tiles; i += EG) {
+      tcx::bar_wait(&d_full[sd], ph);
+      tcx::bar_wait(&n_full[sd], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t dv[32];
+      {
+        uint32_t dw[32];
+        tcx::tmem_ld32(tm + lane_off + dcol0 + (uint32_t)(sd * 64), dv);
+        tcx::tmem_ld32(tm + lane_off + dcol0 + (uint32_t)(sd * 64 + 32), dw);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) dv[j] = __float_as_uint(__uint_as_float(dv[j]) + __uint_as_float(dw[j]));
+      }
+      const float n2 = norms[sd * 128 + r];
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) tcx::bar_arrive(&d_free[sd]);
+      const int64_t row = (int64_t)(t0 + i * tstep) * 128 + r;
+      if (row < n) {
+        // diag (profiling only): >= 2 = no epilogue arithmetic, 1 = selection without the exact recompute
+        const float lam = diag >= 2 ? __uint_as_float(dv[0]) + n2
+                          : diag == 1 ? certified_median<KK, D, KEEP>(dv, n2, cm, gam, nullptr, nullptr, -1, dd, M64)
+                                      : certified_median<KK, D, KEEP>(dv, n2, cm, gam, sA + sa * tile_floats,
+                                                                      A + row * lda, r, dd, M64);
+        lambda[row] = lam;
+        local += (double)lam;
+      }
+      if (KEEP) {
+        __syncwarp();
+        if (lane == 0) tcx::bar_arrive(&a_free[sa]);
+      }
+      sa += EG;
+      while (sa >= NA) sa -= NA;
+      sd += EG;
+      if (sd >= ND) { sd -= ND; ph ^= 1u; }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if (lane == 0) red[warp] = local;
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kEpiWarp0 + 4 * EG; ++w) s += red[w];
+    partial[blockIdx.x] = s;
+  }
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn2() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+constexpr size_t kSmemMax = 232448;   // max dynamic shared memory per block (sm_100)
+
+template <int KK, int D, int EG>
+fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M32, int KP32, const double* M64,
+                  const float* colb, double* partial, int grid, float* lambda, cudaStream_t st) {
+  auto enc = encode_fn2();
+  if (!enc) return FCT_ERR_UNSUPPORTED;
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)n};
+  cuuint64_t strides[1] = {(cuuint64_t)lda * sizeof(float)};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t es[2] = {1, 1};
+  CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)A, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  FCT_CHECK_ARG(cr == CUDA_SUCCESS, FCT_ERR_CUDA, "l1_rownorm: cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  const int nch = (d + 31) / 32, KP = nch * 32;
+  const bool at = 4 * KP + 4 * 64 <= 512 && !getenv("FCT_ROWNORM_ASS");   // A_hi from TMEM when it fits
+  const int ND = std::min(8, (512 - 2 * (at ? 2 * KP : KP)) / 64);
+  int NA = 0;
+  for (int na = 8; na >= 2; --na)
+    if (layout(d, KK, na, ND).total + 1024 <= (int)kSmemMax - 2048) { NA = na; break; }
+  if (NA < 2 || ND < EG + 1) return FCT_ERR_UNSUPPORTED;
+  // keep the tile until the epilogue is done (exact recompute from shared memory) when enough buffers fit
+  const bool keep = NA >= EG + 2 && !getenv("FCT_ROWNORM_NOKEEP");
+  const size_t smem = (size_t)layout(d, KK, NA, ND).total + 1024;
+  const int g = std::max(1, std::min(grid, fct::num_sms()));
+  const int threads = 32 * (kEpiWarp0 + 4 * EG);
+  const float gam = 6.103515625e-05f * 1.05f;   // 3xTF32 bound, 2^-14 (measured 1.9e-6) x 1.05 for roundings
+  auto kern = keep ? (at ? rownorm_ws2_kernel<KK, D, EG, true, true> : rownorm_ws2_kernel<KK, D, EG, true, false>)
+                   : (at ? rownorm_ws2_kernel<KK, D, EG, false, true> : rownorm_ws2_kernel<KK, D, EG, false, false>);
+  FCT_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (fct::debug_sync())
+    fprintf(stderr, "[fct] rownorm_ws2<k=%d,D=%d,EG=%d,keep=%d,at=%d>: grid %d NA %d ND %d smem %zu\n", KK, D, EG,
+            (int)keep, (int)at, g, NA, ND, smem);
+  FCT_CUDA_RET(cudaMemsetAsync(partial, 0, sizeof(double) * grid, st));
+  const char* dg = getenv("FCT_ROWNORM_DIAG");
+  kern<<<g, threads, smem, st>>>(map, A, n, d, lda, M32, KP32, M64, colb, gam, NA, ND, lambda, partial, dg ? atoi(dg) : 0);
+  FCT_LAUNCHED("rownorm_ws2_kernel", st);
+  return FCT_OK;
+}
+
+template <int KK, int DC>
+fct_status launch_k(const float* A, int64_t n, int d, int64_t lda, const float* M32, int KP32, const double* M64,
+                    const float* colb, double* partial, int grid, float* lambda, cudaStream_t st) {
+  const bool eg2 = getenv("FCT_ROWNORM_EG2") != nullptr;
+  if (d == DC)
+    return eg2 ? launch<KK, DC, 2>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st)
+               : launch<KK, DC, 3>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st);
+  return eg2 ? launch<KK, 0, 2>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st)
+             : launch<KK, 0, 3>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st);
+}
+
+}  // namespace
+
+// Returns FCT_ERR_UNSUPPORTED (nothing enqueued) when no instance covers (k, d, alignment).
+// M32: fp32 M~ row-major [d][KP32]; M64: fp64 M row-major [d][k]; colb[2j] = ||m~_j||_2 rounded up.
+// Instances: k of the five BASELINE configurations, each with its config's d unrolled at compile time.
+fct_status fct_rownorm_ws2(const float* A, int64_t n, int d, int64_t lda, const float* M32, int KP32,
+                           const double* M64, const float* colb, int k, double* partial, int grid, float* lambda,
+                           cudaStream_t st) {
+  if (getenv("FCT_ROWNORM_WS1") || getenv("FCT_ROWNORM_SIMT")) return FCT_ERR_UNSUPPORTED;
+  if (d % 4 || d > 128 || lda % 4 || ((uintptr_t)A & 15) || n >= (1LL << 31)) return FCT_ERR_UNSUPPORTED;
+  switch (k) {
+    case 16: return launch_k<16, 8>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st);
+    case 20: return launch_k<20, 16>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st);
+    case 24: return launch_k<24, 32>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st);
+    case 27: return launch_k<27, 64>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st);
+    case 29: return launch_k<29, 100>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st);
+    default: return FCT_ERR_UNSUPPORTED;
+  }
+}

@@ -292,3 +292,25 @@ def test_rownorm_simt_path_matches_too(fct, c, monkeypatch):
     lam, _ = fct.l1_rownorm(dev(B), dev(Rinv), dev(inp.pi2))
     lam = lam.cpu().numpy().astype(np.float64)
     assert (np.abs(lam - lam_o) <= LAM_TOL * lam_o).all()
+
+
+@pytest.mark.parametrize("env", ["FCT_ROWNORM_WS1", "FCT_ROWNORM_EG2", "FCT_ROWNORM_NOKEEP", None])
+@pytest.mark.parametrize("c", [2, 4, 5])
+def test_rownorm_tc_variants(fct, c, env, monkeypatch):
+    """Each tcgen05 row-norm variant (ws2 with 3 or 2 epilogue groups, the older ws) is parity-green,
+    including special rows: zero, tiny (norm underflows in fp32), huge, and a row with exact ties."""
+    if env:
+        monkeypatch.setenv(env, "1")
+    cfg = fctgen.CONFIGS[c]
+    inp = fctgen.make_inputs(cfg, n=2 * cfg.s)
+    Rinv = _rinv_for(inp)
+    B = fctgen.matrix(cfg.kind, cfg.seed, max(cfg.n, 9000), cfg.d, 0, 9000 + 77)
+    B[0] = 0.0
+    B[1] *= np.float32(1e-20)
+    B[2] *= np.float32(1e15)
+    B[3] = 1.0
+    lam_o, _ = oracle.rownorm(B, Rinv, inp.pi2)
+    lam, _ = fct.l1_rownorm(dev(B), dev(Rinv), dev(inp.pi2))
+    lam = lam.cpu().numpy().astype(np.float64)
+    assert lam[0] == 0.0
+    assert (np.abs(lam - lam_o) <= LAM_TOL * lam_o).all()
