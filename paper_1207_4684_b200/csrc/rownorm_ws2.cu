@@ -42,7 +42,7 @@ __device__ __forceinline__ void exact_pair(const float* __restrict__ tile, const
                                           const double* __restrict__ M64, int j0, int j1, double& x0, double& x1) {
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
   const int dd = D ? D : d;
-#pragma unroll(D ? D / 4 : 1)
+#pragma unroll 4
   for (int l = 0; l < dd; l += 4) {
     const float4 a = KEEP ? *(const float4*)(tile + tcx::sw_off(r, l)) : __ldg((const float4*)(grow + l));
     const double d0 = a.x, d1 = a.y, d2 = a.z, d3 = a.w;
@@ -58,6 +58,50 @@ __device__ __forceinline__ void exact_pair(const float* __restrict__ tile, const
   }
   x0 = fabs((a0 + a1) + (a2 + a3));
   x1 = fabs((b0 + b1) + (b2 + b3));
+}
+
+// rare: several candidates -- exact value of each, then rank by counting (ties broken by index); out of line
+template <int KK, int D, bool KEEP>
+__device__ __noinline__ void rare_candidates(const float* __restrict__ tile, const float* __restrict__ grow, int r, int d,
+                                             const double* __restrict__ M64, unsigned cmask, int q1, int q2, double& x1,
+                                             double& x2) {
+  double ex[KK];
+  x1 = x2 = 0.0;
+#pragma unroll 1
+  for (int j = 0; j < KK; ++j) {
+    ex[j] = 0.0;
+    if ((cmask >> j) & 1u) {
+      double c0, c1;
+      exact_pair<KK, D, KEEP>(tile, grow, r, d, M64, j, j, c0, c1);
+      ex[j] = c0;
+    }
+  }
+#pragma unroll 1
+  for (int a = 0; a < KK; ++a) {
+    if (!((cmask >> a) & 1u)) continue;
+    int rank = 0;
+    for (int b = 0; b < KK; ++b) rank += ((cmask >> b) & 1u) && (ex[b] < ex[a] || (ex[b] == ex[a] && b < a));
+    if (rank == q1) x1 = ex[a];
+    if (rank == q2) x2 = ex[a];
+  }
+}
+
+// exact |sum_l a_l M_lj| for one column j (fp64)
+template <int KK, int D, bool KEEP>
+__device__ __forceinline__ double exact_one(const float* __restrict__ tile, const float* __restrict__ grow, int r, int d,
+                                            const double* __restrict__ M64, int j) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const int dd = D ? D : d;
+#pragma unroll 4
+  for (int l = 0; l < dd; l += 4) {
+    const float4 a = KEEP ? *(const float4*)(tile + tcx::sw_off(r, l)) : __ldg((const float4*)(grow + l));
+    const double* m = M64 + (size_t)l * KK + j;
+    a0 = fma((double)a.x, m[0], a0);
+    a1 = fma((double)a.y, m[KK], a1);
+    a2 = fma((double)a.z, m[2 * KK], a2);
+    a3 = fma((double)a.w, m[3 * KK], a3);
+  }
+  return fabs((a0 + a1) + (a2 + a3));
 }
 
 template <int KK, int D, bool KEEP>
@@ -103,36 +147,18 @@ __device__ __forceinline__ float certified_median(const uint32_t (&dv)[32], floa
   const int nc = __popc(cmask);
   if (r < 0) return v1 + v2 + (float)nc;   // diag
   double x1, x2;
-  if (nc <= 2) {
+  if (nc == 1) {
+    x1 = x2 = exact_one<KK, D, KEEP>(tile, grow, r, d, M64, __ffs(cmask) - 1);
+  } else if (nc == 2) {
     const int j0 = __ffs(cmask) - 1;
-    const int j1 = nc == 2 ? 31 - __clz(cmask) : j0;
+    const int j1 = 31 - __clz(cmask);
     double c0, c1;
     exact_pair<KK, D, KEEP>(tile, grow, r, d, M64, j0, j1, c0, c1);
     const double cmin = fmin(c0, c1), cmax = fmax(c0, c1);
     x1 = q1 == 0 ? cmin : cmax;
     x2 = q2 == 0 ? cmin : cmax;
   } else {
-    // rare: several candidates -- exact value of each, then rank by counting (ties broken by index)
-    double ex[KK];
-    x1 = x2 = 0.0;
-#pragma unroll 1
-    for (int j = 0; j < KK; ++j) {
-      ex[j] = 0.0;
-      if ((cmask >> j) & 1u) {
-        double c0, c1;
-        exact_pair<KK, D, KEEP>(tile, grow, r, d, M64, j, j, c0, c1);
-        ex[j] = c0;
-      }
-    }
-#pragma unroll 1
-    for (int a = 0; a < KK; ++a) {
-      if (!((cmask >> a) & 1u)) continue;
-      int rank = 0;
-      for (int b = 0; b < KK; ++b)
-        rank += ((cmask >> b) & 1u) && (ex[b] < ex[a] || (ex[b] == ex[a] && b < a));
-      if (rank == q1) x1 = ex[a];
-      if (rank == q2) x2 = ex[a];
-    }
+    rare_candidates<KK, D, KEEP>(tile, grow, r, d, M64, cmask, q1, q2, x1, x2);
   }
   return (float)(0.5 * (x1 + x2));
 }
@@ -354,9 +380,8 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
       if (row < n) {
         // diag (profiling only): >= 2 = no epilogue arithmetic, 1 = selection without the exact recompute
         const float lam = diag >= 2 ? __uint_as_float(dv[0]) + n2
-                          : diag == 1 ? certified_median<KK, D, KEEP>(dv, n2, cm, gam, nullptr, nullptr, -1, dd, M64)
-                                      : certified_median<KK, D, KEEP>(dv, n2, cm, gam, sA + sa * tile_floats,
-                                                                      A + row * lda, r, dd, M64);
+                                    : certified_median<KK, D, KEEP>(dv, n2, cm, gam, sA + sa * tile_floats,
+                                                                    A + row * lda, diag == 1 ? -1 : r, dd, M64);
         lambda[row] = lam;
         local += (double)lam;
       }

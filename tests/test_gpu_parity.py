@@ -309,6 +309,7 @@ def test_rownorm_tc_variants(fct, c, env, monkeypatch):
     B[1] *= np.float32(1e-20)
     B[2] *= np.float32(1e15)
     B[3] = 1.0
+    B[4, ::3] = np.float32(3e-39)                   # subnormal entries (exact fp64 conversion path)
     lam_o, _ = oracle.rownorm(B, Rinv, inp.pi2)
     lam, _ = fct.l1_rownorm(dev(B), dev(Rinv), dev(inp.pi2))
     lam = lam.cpu().numpy().astype(np.float64)
