@@ -315,3 +315,19 @@ def test_rownorm_tc_variants(fct, c, env, monkeypatch):
     lam = lam.cpu().numpy().astype(np.float64)
     assert lam[0] == 0.0
     assert (np.abs(lam - lam_o) <= LAM_TOL * lam_o).all()
+
+
+@pytest.mark.parametrize("c", [1, 3, 4, 5])
+def test_sketch_hot_buckets(fct, c):
+    """Adversarial hashes that put most H~-rows of every block into a handful of buckets: the shared-memory
+    CAS scatter retries constantly and every update must still land exactly once."""
+    cfg = fctgen.CONFIGS[c]
+    inp = fctgen.make_inputs(cfg, n=7 * cfg.s + 19)
+    Yo, Mb = oracle.sketch(inp.A, inp.signs, inp.cauchy, inp.hash, cfg.s, cfg.r1)
+    assert_sketch_close(sketch_gpu(fct, inp), Yo, Mb)
+    hot = inp.hash.copy()
+    hot[::2] %= 8                      # half of all H~-rows in 8 hot buckets
+    hot[1::4] = 11 % cfg.r1            # a quarter in one bucket
+    inp.hash = hot
+    Yo2, Mb2 = oracle.sketch(inp.A, inp.signs, inp.cauchy, inp.hash, cfg.s, cfg.r1)
+    assert_sketch_close(sketch_gpu(fct, inp), Yo2, Mb2)
