@@ -104,11 +104,13 @@ __device__ __forceinline__ double exact_one(const float* __restrict__ tile, cons
   return fabs((a0 + a1) + (a2 + a3));
 }
 
+// Selection half of the certified median (no fp64 work unless the row is degenerate): returns true with
+// lam set when the row is settled here (1-2 candidates are handed on as a descriptor otherwise):
+//   desc = j0 | j1 << 5 | q1 << 10 | q2 << 15 | (nc - 1) << 20
 template <int KK, int D, bool KEEP>
-__device__ __forceinline__ float certified_median(const uint32_t (&dv)[32], float n2, const float* __restrict__ cm,
-                                                  float gam, const float* __restrict__ tile,
-                                                  const float* __restrict__ grow, int r, int d,
-                                                  const double* __restrict__ M64) {
+__device__ __forceinline__ bool certify(const uint32_t (&dv)[32], float n2, const float* __restrict__ cm, float gam,
+                                        const float* __restrict__ tile, const float* __restrict__ grow, int r, int d,
+                                        const double* __restrict__ M64, float& lam, uint32_t& desc) {
   constexpr int m1 = (KK - 1) / 2, m2 = KK / 2;
   float v[KK], srt[KK];
   const float g = gam * __fsqrt_ru(n2);
@@ -145,27 +147,33 @@ __device__ __forceinline__ float certified_median(const uint32_t (&dv)[32], floa
   }
   const int q1 = m1 - below, q2 = m2 - below;
   const int nc = __popc(cmask);
-  if (r < 0) return v1 + v2 + (float)nc;   // diag
-  double x1, x2;
-  if (nc == 1) {
-    x1 = x2 = exact_one<KK, D, KEEP>(tile, grow, r, d, M64, __ffs(cmask) - 1);
-  } else if (nc == 2) {
-    const int j0 = __ffs(cmask) - 1;
-    const int j1 = 31 - __clz(cmask);
-    double c0, c1;
-    exact_pair<KK, D, KEEP>(tile, grow, r, d, M64, j0, j1, c0, c1);
-    const double cmin = fmin(c0, c1), cmax = fmax(c0, c1);
-    x1 = q1 == 0 ? cmin : cmax;
-    x2 = q2 == 0 ? cmin : cmax;
-  } else {
-    rare_candidates<KK, D, KEEP>(tile, grow, r, d, M64, cmask, q1, q2, x1, x2);
+  if (nc <= 2) {
+    const int j0 = __ffs(cmask) - 1, j1 = 31 - __clz(cmask);
+    desc = (uint32_t)j0 | ((uint32_t)j1 << 5) | ((uint32_t)q1 << 10) | ((uint32_t)q2 << 15) | ((uint32_t)(nc - 1) << 20);
+    return false;
   }
-  return (float)(0.5 * (x1 + x2));
+  double x1, x2;
+  rare_candidates<KK, D, KEEP>(tile, grow, r, d, M64, cmask, q1, q2, x1, x2);
+  lam = (float)(0.5 * (x1 + x2));
+  return true;
+}
+
+// fp64 half: exact values of the 1-2 candidates of a descriptor, ranked
+template <int KK, int D, bool KEEP>
+__device__ __forceinline__ float resolve(uint32_t desc, const float* __restrict__ tile, const float* __restrict__ grow,
+                                         int r, int d, const double* __restrict__ M64) {
+  const int j0 = desc & 31, j1 = (desc >> 5) & 31, q1 = (desc >> 10) & 31, q2 = (desc >> 15) & 31;
+  if (!((desc >> 20) & 1u)) return (float)exact_one<KK, D, KEEP>(tile, grow, r, d, M64, j0);
+  double c0, c1;
+  exact_pair<KK, D, KEEP>(tile, grow, r, d, M64, j0, j1, c0, c1);
+  const double cmin = fmin(c0, c1), cmax = fmax(c0, c1);
+  return (float)(0.5 * ((q1 == 0 ? cmin : cmax) + (q2 == 0 ? cmin : cmax)));
 }
 
 struct Smem {   // byte offsets inside the 1024-aligned dynamic shared memory
-  int a, b, m64, cm, nrm, bars, total;
+  int a, b, m64, cm, nrm, cq, bars, total;
 };
+constexpr int kCQ = 4;   // candidate-descriptor ring (selection -> recompute warps)
 __host__ __device__ inline Smem layout(int d, int KK, int NA, int ND) {
   const int nch = (d + 31) / 32;
   Smem s;
@@ -174,8 +182,9 @@ __host__ __device__ inline Smem layout(int d, int KK, int NA, int ND) {
   s.m64 = s.b + nch * 8192;
   s.cm = s.m64 + ((d * KK * 8 + 15) & ~15);
   s.nrm = s.cm + 32 * 4;
-  s.bars = s.nrm + ND * 128 * 4;
-  s.total = s.bars + 8 * (2 * NA + 4 + 3 * ND);
+  s.cq = s.nrm + ND * 128 * 4;           // [kCQ][128] descriptors + [kCQ][128] settled lambdas
+  s.bars = s.cq + kCQ * 128 * 8;
+  s.total = s.bars + 8 * (2 * NA + 4 + 3 * ND + 2 * kCQ);
   return s;
 }
 
@@ -183,8 +192,8 @@ __host__ __device__ inline Smem layout(int d, int KK, int NA, int ND) {
 template <bool AT>
 __host__ __device__ inline int abuf_cols(int KP) { return AT ? 2 * KP : KP; }
 
-template <int KK, int D, int EG, bool KEEP, bool AT>
-__global__ void __launch_bounds__(32 * (kEpiWarp0 + 4 * EG), 1)
+template <int KK, int D, int EG, int RG, bool KEEP, bool AT>
+__global__ void __launch_bounds__(32 * (kEpiWarp0 + 4 * EG + 4 * RG), 1)
 rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ A, int64_t n, int d, int64_t lda,
                    const float* __restrict__ M32g, int KP32, const double* __restrict__ M64g,
                    const float* __restrict__ colbg, float gam, int NA, int ND, float* __restrict__ lambda,
@@ -207,14 +216,19 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
   uint64_t* d_full = at_free + 2;                     // [ND]  accumulator ready
   uint64_t* n_full = d_full + ND;                     // [ND]  norms written (4 split-warp arrivals)
   uint64_t* d_free = n_full + ND;                     // [ND]  accumulator + norms drained (4 warp arrivals)
+  uint64_t* c_full = d_free + ND;                     // [kCQ] descriptors written (4 selection-warp arrivals)
+  uint64_t* c_free = c_full + kCQ;                    // [kCQ] descriptors consumed (4 recompute-warp arrivals)
+  uint32_t* cdesc = (uint32_t*)(base + L.cq);
+  float* clam = (float*)(cdesc + kCQ * 128);
+  constexpr int NWARPS = kEpiWarp0 + 4 * EG + 4 * RG;
   __shared__ uint32_t tbase;
-  __shared__ double red[kEpiWarp0 + 4 * EG];
+  __shared__ double red[NWARPS];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   if (tid == 0) {
     for (int i = 0; i < NA; ++i) {
       tcx::bar_init(&tma_full[i], 1);
-      tcx::bar_init(&a_free[i], KEEP ? 4 : 1);
+      tcx::bar_init(&a_free[i], KEEP ? 4 : 1);   // KEEP: released by the warps that finish the tile's rows
     }
     for (int i = 0; i < 2; ++i) {
       tcx::bar_init(&at_full[i], 4);
@@ -224,6 +238,10 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
       tcx::bar_init(&d_full[i], 1);
       tcx::bar_init(&n_full[i], 4);
       tcx::bar_init(&d_free[i], 4);
+    }
+    for (int i = 0; i < kCQ; ++i) {
+      tcx::bar_init(&c_full[i], 4);
+      tcx::bar_init(&c_free[i], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -351,15 +369,15 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
         if (++sd == ND) { sd = 0; pd ^= 1u; }
       }
     }
-  } else {
-    // ------------------------------------------------------------------ epilogue groups
+  } else if (warp < kEpiWarp0 + 4 * EG) {
+    // ------------------------------------------------------------------ selection (epilogue) groups
     const int ew = warp - kEpiWarp0;
     const int g = ew >> 2;
     const int quad = warp & 3;                        // TMEM lane quadrant this warp may access
     const int r = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    int sd = g % ND, sa = g % NA;
-    unsigned ph = (unsigned)((g / ND) & 1);
+    int sd = g % ND, sa = g % NA, cs = g % kCQ;
+    unsigned ph = (unsigned)((g / ND) & 1), pc = (unsigned)((g / kCQ) & 1);
     for (int i = g; i < my_tiles; i += EG) {
       tcx::bar_wait(&d_full[sd], ph);
       tcx::bar_wait(&n_full[sd], ph);
@@ -377,11 +395,54 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
       __syncwarp();
       if (lane == 0) tcx::bar_arrive(&d_free[sd]);
       const int64_t row = (int64_t)(t0 + i * tstep) * 128 + r;
+      const float* tile = sA + sa * tile_floats;
+      float lam = 0.f;
+      uint32_t desc = 0u;
+      bool fin = true;
       if (row < n) {
-        // diag (profiling only): >= 2 = no epilogue arithmetic, 1 = selection without the exact recompute
-        const float lam = diag >= 2 ? __uint_as_float(dv[0]) + n2
-                                    : certified_median<KK, D, KEEP>(dv, n2, cm, gam, sA + sa * tile_floats,
-                                                                    A + row * lda, diag == 1 ? -1 : r, dd, M64);
+        if (diag >= 2) lam = __uint_as_float(dv[0]) + n2;   // diag (profiling only): no epilogue arithmetic
+        else fin = certify<KK, D, KEEP>(dv, n2, cm, gam, tile, A + row * lda, r, dd, M64, lam, desc);
+      }
+      if (RG == 0) {
+        if (row < n) {
+          if (!fin) lam = diag == 1 ? 0.f : resolve<KK, D, KEEP>(desc, tile, A + row * lda, r, dd, M64);
+          lambda[row] = lam;
+          local += (double)lam;
+        }
+        if (KEEP) {
+          __syncwarp();
+          if (lane == 0) tcx::bar_arrive(&a_free[sa]);
+        }
+      } else {
+        if (i >= kCQ) tcx::bar_wait(&c_free[cs], pc ^ 1u);
+        cdesc[cs * 128 + r] = fin ? 0x80000000u : desc;
+        clam[cs * 128 + r] = lam;
+        __syncwarp();
+        if (lane == 0) tcx::bar_arrive(&c_full[cs]);
+      }
+      sa += EG;
+      while (sa >= NA) sa -= NA;
+      sd += EG;
+      if (sd >= ND) { sd -= ND; ph ^= 1u; }
+      cs += EG;
+      while (cs >= kCQ) { cs -= kCQ; pc ^= 1u; }
+    }
+  } else {
+    // ------------------------------------------------------------------ recompute groups (RG > 0)
+    const int rw = warp - kEpiWarp0 - 4 * EG;
+    const int g = rw >> 2;
+    const int r = (rw & 3) * 32 + lane;
+    int sa = g % NA, cs = g % kCQ;
+    unsigned pc = (unsigned)((g / kCQ) & 1);
+    for (int i = g; i < my_tiles; i += RG) {
+      tcx::bar_wait(&c_full[cs], pc);
+      const uint32_t desc = cdesc[cs * 128 + r];
+      float lam = clam[cs * 128 + r];
+      __syncwarp();
+      if (lane == 0) tcx::bar_arrive(&c_free[cs]);
+      const int64_t row = (int64_t)(t0 + i * tstep) * 128 + r;
+      if (row < n) {
+        if (!(desc >> 31) && diag != 1) lam = resolve<KK, D, KEEP>(desc, sA + sa * tile_floats, A + row * lda, r, dd, M64);
         lambda[row] = lam;
         local += (double)lam;
       }
@@ -389,10 +450,10 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
         __syncwarp();
         if (lane == 0) tcx::bar_arrive(&a_free[sa]);
       }
-      sa += EG;
+      sa += RG;
       while (sa >= NA) sa -= NA;
-      sd += EG;
-      if (sd >= ND) { sd -= ND; ph ^= 1u; }
+      cs += RG;
+      while (cs >= kCQ) { cs -= kCQ; pc ^= 1u; }
     }
   }
   for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
@@ -401,7 +462,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
   __syncthreads();
   if (tid == 0) {
     double s = 0.0;
-    for (int w = 0; w < kEpiWarp0 + 4 * EG; ++w) s += red[w];
+    for (int w = 0; w < NWARPS; ++w) s += red[w];
     partial[blockIdx.x] = s;
   }
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
@@ -421,7 +482,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn2() {
 
 constexpr size_t kSmemMax = 232448;   // max dynamic shared memory per block (sm_100)
 
-template <int KK, int D, int EG>
+template <int KK, int D, int EG, int RG>
 fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M32, int KP32, const double* M64,
                   const float* colb, double* partial, int grid, float* lambda, cudaStream_t st) {
   auto enc = encode_fn2();
@@ -444,16 +505,17 @@ fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M3
   if (NA < 2 || ND < EG + 1) return FCT_ERR_UNSUPPORTED;
   // keep the tile until the epilogue is done (exact recompute from shared memory) when enough buffers fit
   const bool keep = NA >= EG + 2 && !getenv("FCT_ROWNORM_NOKEEP");
+  if (RG > 0 && !keep) return FCT_ERR_UNSUPPORTED;
   const size_t smem = (size_t)layout(d, KK, NA, ND).total + 1024;
   const int g = std::max(1, std::min(grid, fct::num_sms()));
-  const int threads = 32 * (kEpiWarp0 + 4 * EG);
+  const int threads = 32 * (kEpiWarp0 + 4 * EG + 4 * RG);
   const float gam = 6.103515625e-05f * 1.05f;   // 3xTF32 bound, 2^-14 (measured 1.9e-6) x 1.05 for roundings
-  auto kern = keep ? (at ? rownorm_ws2_kernel<KK, D, EG, true, true> : rownorm_ws2_kernel<KK, D, EG, true, false>)
-                   : (at ? rownorm_ws2_kernel<KK, D, EG, false, true> : rownorm_ws2_kernel<KK, D, EG, false, false>);
+  auto kern = keep ? (at ? rownorm_ws2_kernel<KK, D, EG, RG, true, true> : rownorm_ws2_kernel<KK, D, EG, RG, true, false>)
+                   : (at ? rownorm_ws2_kernel<KK, D, EG, RG, false, true> : rownorm_ws2_kernel<KK, D, EG, RG, false, false>);
   FCT_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (fct::debug_sync())
-    fprintf(stderr, "[fct] rownorm_ws2<k=%d,D=%d,EG=%d,keep=%d,at=%d>: grid %d NA %d ND %d smem %zu\n", KK, D, EG,
-            (int)keep, (int)at, g, NA, ND, smem);
+    fprintf(stderr, "[fct] rownorm_ws2<k=%d,D=%d,EG=%d,RG=%d,keep=%d,at=%d>: grid %d NA %d ND %d smem %zu\n", KK, D, EG,
+            RG, (int)keep, (int)at, g, NA, ND, smem);
   FCT_CUDA_RET(cudaMemsetAsync(partial, 0, sizeof(double) * grid, st));
   const char* dg = getenv("FCT_ROWNORM_DIAG");
   kern<<<g, threads, smem, st>>>(map, A, n, d, lda, M32, KP32, M64, colb, gam, NA, ND, lambda, partial, dg ? atoi(dg) : 0);
@@ -464,12 +526,21 @@ fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M3
 template <int KK, int DC>
 fct_status launch_k(const float* A, int64_t n, int d, int64_t lda, const float* M32, int KP32, const double* M64,
                     const float* colb, double* partial, int grid, float* lambda, cudaStream_t st) {
-  const bool eg2 = getenv("FCT_ROWNORM_EG2") != nullptr;
-  if (d == DC)
-    return eg2 ? launch<KK, DC, 2>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st)
-               : launch<KK, DC, 3>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st);
-  return eg2 ? launch<KK, 0, 2>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st)
-             : launch<KK, 0, 3>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st);
+  // variants (FCT_ROWNORM_VAR): 0 = 2 selection + 2 recompute groups, 1 = 3 groups that also (default)
+  // recompute, 2 = 2 groups that also recompute
+  const char* ve = getenv("FCT_ROWNORM_VAR");
+  const int var = ve ? atoi(ve) : (getenv("FCT_ROWNORM_EG2") ? 2 : 1);
+#define FCT_RN_LAUNCH(DD)                                                                                  \
+  do {                                                                                                     \
+    fct_status rc_ = FCT_ERR_UNSUPPORTED;                                                                  \
+    if (var == 0) rc_ = launch<KK, DD, 2, 2>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st); \
+    if (rc_ != FCT_ERR_UNSUPPORTED) return rc_;                                                            \
+    if (var == 2) return launch<KK, DD, 2, 0>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st); \
+    return launch<KK, DD, 3, 0>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st);            \
+  } while (0)
+  if (d == DC) FCT_RN_LAUNCH(DC);
+  FCT_RN_LAUNCH(0);
+#undef FCT_RN_LAUNCH
 }
 
 }  // namespace
