@@ -136,6 +136,18 @@ fct_status l1_sample_u(const float* p, const double* u, int64_t n, int64_t row_b
                        int64_t m, int64_t* idx, double* weight, int64_t capacity,
                        int64_t* count, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Fused a9 + a10 (what the pipeline runs): p[i] = (float)((double)lambda[i] / *lambda_total)
+ * exactly as l1_probs, then the Bernoulli sampling of l1_sample on that p, in ONE pass over
+ * lambda (single-pass decoupled look-back compaction).  Outputs (p, idx, weight, count) are
+ * bit-identical to l1_probs followed by l1_sample.  workspace: l1_probs_sample_workspace_bytes(n)
+ * device bytes (zeroed by the call, on `stream`).  Errors as l1_sample.
+ */
+size_t l1_probs_sample_workspace_bytes(int64_t n);
+fct_status l1_probs_sample(const float* lambda, int64_t n, const double* lambda_total,
+                           int64_t row_base, int64_t m, uint64_t seed, float* p, int64_t* idx,
+                           double* weight, int64_t capacity, int64_t* count, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------------------------------------
  * Whole single-device hot path: sketch -> condition -> row-norm ->
  * probabilities -> sample, all enqueued on `stream` (device pointers).  Y (r1 x d fp32),

@@ -11,6 +11,7 @@ from .api import (  # noqa: F401
     fct_condition,
     fct_sketch,
     l1_probs,
+    l1_probs_sample,
     l1_rownorm,
     l1_rownorm_probs,
     l1_sample,

@@ -169,6 +169,25 @@ def l1_sample_u(p, u, m: int, row_base: int = 0, capacity: int | None = None):
     return _sample(p, m, 0, row_base, capacity, u)
 
 
+def l1_probs_sample(lam, lambda_total, m: int, seed: int, row_base: int = 0, capacity: int | None = None):
+    """Fused probabilities + Bernoulli sampling (one pass over lambda).
+    Returns (p, idx[capacity], weight[capacity], count[1]) device tensors."""
+    L = _lib_()
+    _need(lam, torch.float32, "lambda")
+    _need(lambda_total, torch.float64, "lambda_total")
+    n = lam.numel()
+    cap = 2 * m + 64 if capacity is None else capacity
+    p = torch.empty_like(lam)
+    idx = torch.empty(max(cap, 1), dtype=torch.int64, device=lam.device)
+    w = torch.empty(max(cap, 1), dtype=torch.float64, device=lam.device)
+    cnt = torch.zeros(1, dtype=torch.int64, device=lam.device)
+    nb = L.l1_probs_sample_workspace_bytes(n)
+    ws = workspace(nb, "probs_sample")
+    _lib.check(L.l1_probs_sample(_ptr(lam), n, _ptr(lambda_total), row_base, m, seed & 0xFFFFFFFFFFFFFFFF, _ptr(p),
+                                 _ptr(idx), _ptr(w), cap, _ptr(cnt), _ptr(ws), ws.numel(), _stream()))
+    return p, idx, w, cnt
+
+
 def trim(idx, w, cnt):
     """Host copies of the first min(count, capacity) samples."""
     c = int(cnt.item())

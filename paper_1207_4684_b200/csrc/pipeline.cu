@@ -11,7 +11,7 @@ PipeWS pipe_ws(int64_t n, int64_t d, int32_t s, int32_t r1, int32_t k) {
   w.sketch = fct::align256(fct_sketch_workspace_bytes(n, d, s, r1));
   w.cond = fct::align256(fct_condition_workspace_bytes(r1, d));
   w.rown = fct::align256(l1_rownorm_workspace_bytes(n, d, k));
-  w.samp = fct::align256(l1_sample_workspace_bytes(n));
+  w.samp = fct::align256(std::max(l1_sample_workspace_bytes(n), l1_probs_sample_workspace_bytes(n)));
   w.total = w.sketch + w.cond + w.rown + w.samp + fct::align256(sizeof(double));
   return w;
 }
@@ -46,8 +46,7 @@ extern "C" fct_status fct_pipeline(const float* A, int64_t n, int64_t d, int64_t
   if ((rc = fct_condition(Y, r1, d, R, Rinv, info, ws_cd, w.cond, stream)) != FCT_OK) return rc;
   if ((rc = fct_rownorm_impl(A, n, d, lda, Rinv, Pi2, k, lambda, total, true, ws_rn, w.rown, st)) != FCT_OK)
     return rc;
-  if ((rc = l1_probs(lambda, n, total, p, stream)) != FCT_OK) return rc;
-  return l1_sample(p, n, 0, m, seed, idx, weight, capacity, count, ws_sp, w.samp, stream);
+  return l1_probs_sample(lambda, n, total, 0, m, seed, p, idx, weight, capacity, count, ws_sp, w.samp, stream);
 }
 
 // ------------------------------------------------------------------------------ host-buffer variant

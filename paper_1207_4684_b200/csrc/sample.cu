@@ -31,6 +31,13 @@ struct Decide {
     else ui = (double)(mix64(key + 0x9E3779B97F4A7C15ULL * (uint64_t)(row_base + i + 1)) >> 11) * 0x1.0p-53;
     return ui < phat;
   }
+  // the same decision from an already-rounded p value
+  __device__ __forceinline__ bool decide_p(float pi, int64_t i, double& phat) const {
+    const double mp = m * (double)pi;
+    phat = mp < 1.0 ? mp : 1.0;
+    const double ui = (double)(mix64(key + 0x9E3779B97F4A7C15ULL * (uint64_t)(row_base + i + 1)) >> 11) * 0x1.0p-53;
+    return ui < phat;
+  }
 };
 
 __global__ void __launch_bounds__(kThreads) count_kernel(Decide dec, int64_t n, int64_t* __restrict__ counts) {
@@ -129,6 +136,121 @@ __global__ void __launch_bounds__(kThreads) write_kernel(Decide dec, int64_t n, 
   }
 }
 
+
+// ------------------------------------------------------------------------------------------------
+// Single-pass fused probabilities + sampling for the pipeline (a9 + a10 in one kernel):
+//   p_i = (float)((double)lambda_i / total)   (exactly l1_probs), then the same exact fp64 decision and
+//   ascending compaction as count/scan/write, with the tile offsets from a decoupled look-back:
+// tile t (taken in launch order from an atomic ticket, so every predecessor is already running)
+// publishes its count as an AGGREGATE, walks back over predecessors summing aggregates until it meets an
+// INCLUSIVE prefix, publishes its own INCLUSIVE prefix and writes its kept rows.  Integer arithmetic
+// only -> idx / weight / count bit-identical to the three-kernel path.  Reads lambda once, writes p once.
+constexpr uint64_t kAgg = 1ull << 62, kInc = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kThreads) probs_sample_kernel(const float* __restrict__ lambda,
+                                                                 const double* __restrict__ total, float* __restrict__ p,
+                                                                 Decide dec, int64_t n, int64_t ntiles,
+                                                                 unsigned long long* __restrict__ state,
+                                                                 unsigned* __restrict__ ticket, int64_t* __restrict__ idx,
+                                                                 double* __restrict__ weight, int64_t capacity,
+                                                                 int64_t* __restrict__ count, int vec) {
+  __shared__ int64_t s_tile, s_excl;
+  __shared__ int wt[kThreads / 32];
+  if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const double tot = *total;
+  const int64_t base = tile * kTile + (int64_t)threadIdx.x * kRowsPerThread;
+  unsigned keep = 0u;
+  double ph[kRowsPerThread];
+  float pv[kRowsPerThread];
+  if (vec && base + kRowsPerThread <= n) {
+    const float4 l0 = *(const float4*)(lambda + base), l1 = *(const float4*)(lambda + base + 4);
+    const float lv[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+#pragma unroll
+    for (int r = 0; r < kRowsPerThread; ++r) pv[r] = (float)((double)lv[r] / tot);
+    *(float4*)(p + base) = make_float4(pv[0], pv[1], pv[2], pv[3]);
+    *(float4*)(p + base + 4) = make_float4(pv[4], pv[5], pv[6], pv[7]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < kRowsPerThread; ++r) {
+      pv[r] = 0.f;
+      if (base + r < n) {
+        pv[r] = (float)((double)lambda[base + r] / tot);
+        p[base + r] = pv[r];
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kRowsPerThread; ++r) {
+    const int64_t i = base + r;
+    ph[r] = 1.0;
+    if (i < n && dec.decide_p(pv[r], i, ph[r])) keep |= 1u << r;
+  }
+  const int c = __popc(keep);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wt[warp] = x;
+  __syncthreads();
+  int wpre = 0, agg = 0;
+  for (int w = 0; w < kThreads / 32; ++w) {
+    if (w < warp) wpre += wt[w];
+    agg += wt[w];
+  }
+  if (warp == 0) {
+    // warp-parallel look-back: lane j inspects tile (t - 1 - j) of the current window of 32
+    volatile unsigned long long* st = state;
+    if (tile == 0) {
+      if (lane == 0) {
+        st[0] = kInc | (uint64_t)agg;
+        s_excl = 0;
+      }
+    } else {
+      if (lane == 0) {
+        st[tile] = kAgg | (uint64_t)agg;
+        __threadfence();
+      }
+      __syncwarp();
+      int64_t excl = 0;
+      int64_t t = tile - 1 - lane;
+      while (true) {
+        uint64_t v = kInc;   // past tile 0: nothing to add, acts as the terminating prefix
+        if (t >= 0)
+          do { v = st[t]; } while ((v >> 62) == 0);
+        const unsigned inc = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+        const int stop = inc ? __ffs(inc) - 1 : 32;          // nearest inclusive prefix in the window
+        int64_t add = (lane <= stop && t >= 0) ? (int64_t)(v & kValMask) : 0;
+        for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+        excl += add;
+        if (inc) break;
+        t -= 32;
+      }
+      if (lane == 0) {
+        __threadfence();
+        st[tile] = kInc | (uint64_t)(excl + agg);
+        s_excl = excl;
+      }
+    }
+    if (lane == 0 && tile == ntiles - 1) *count = s_excl + agg;
+  }
+  __syncthreads();
+  int64_t pos = s_excl + wpre + x - c;
+#pragma unroll
+  for (int r = 0; r < kRowsPerThread; ++r) {
+    if ((keep >> r) & 1u) {
+      if (pos < capacity) {
+        idx[pos] = dec.row_base + base + r;
+        weight[pos] = 1.0 / ph[r];
+      }
+      ++pos;
+    }
+  }
+}
+
 fct_status sample_impl(const float* p, const double* u, int64_t n, int64_t row_base, int64_t m, uint64_t seed,
                        int64_t* idx, double* weight, int64_t capacity, int64_t* count, void* ws, size_t wsb,
                        cudaStream_t st) {
@@ -171,4 +293,35 @@ extern "C" fct_status l1_sample_u(const float* p, const double* u, int64_t n, in
   FCT_CHECK_ARG(u, FCT_ERR_ARG, "l1_sample_u: u is NULL");
   return sample_impl(p, u, n, row_base, m, 0, idx, weight, capacity, count, workspace, workspace_bytes,
                      (cudaStream_t)stream);
+}
+
+extern "C" size_t l1_probs_sample_workspace_bytes(int64_t n) {
+  if (n < 1) return 0;
+  return fct::align256(sizeof(unsigned long long) * (size_t)((n + kTile - 1) / kTile)) + fct::align256(sizeof(unsigned));
+}
+
+extern "C" fct_status l1_probs_sample(const float* lambda, int64_t n, const double* lambda_total, int64_t row_base,
+                                      int64_t m, uint64_t seed, float* p, int64_t* idx, double* weight,
+                                      int64_t capacity, int64_t* count, void* workspace, size_t workspace_bytes,
+                                      void* stream) {
+  FCT_CHECK_ARG(lambda && lambda_total && p && count && (capacity == 0 || (idx && weight)), FCT_ERR_ARG,
+                "l1_probs_sample: NULL pointer");
+  FCT_CHECK_ARG(n >= 1 && row_base >= 0 && capacity >= 0, FCT_ERR_SHAPE, "l1_probs_sample: n=%lld row_base=%lld",
+                (long long)n, (long long)row_base);
+  FCT_CHECK_ARG(m >= 1 && m <= (1LL << 29), FCT_ERR_ARG, "l1_probs_sample: m=%lld not in [1, 2^29]", (long long)m);
+  const size_t need = l1_probs_sample_workspace_bytes(n);
+  FCT_CHECK_ARG(workspace && workspace_bytes >= need, FCT_ERR_WORKSPACE, "l1_probs_sample: workspace %zu < %zu bytes",
+                workspace_bytes, need);
+  const int64_t ntiles = (n + kTile - 1) / kTile;
+  FCT_CHECK_ARG(ntiles <= 0x7fffffffLL, FCT_ERR_SHAPE, "l1_probs_sample: n too large");
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* state = (unsigned long long*)workspace;
+  unsigned* ticket = (unsigned*)((char*)workspace + fct::align256(sizeof(unsigned long long) * (size_t)ntiles));
+  FCT_CUDA_RET(cudaMemsetAsync(workspace, 0, need, st));
+  Decide dec{nullptr, nullptr, row_base, (double)m, mix64(seed + 0x9E3779B97F4A7C15ULL * 10ULL)};
+  probs_sample_kernel<<<(unsigned)ntiles, kThreads, 0, st>>>(lambda, lambda_total, p, dec, n, ntiles, state, ticket,
+                                                              idx, weight, capacity, count,
+                                                              (((uintptr_t)lambda | (uintptr_t)p) & 15) == 0);
+  FCT_LAUNCHED("probs_sample_kernel", st);
+  return FCT_OK;
 }

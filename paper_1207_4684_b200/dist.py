@@ -46,6 +46,7 @@ class Ops:
     rownorm: Callable     # (A, Rinv, Pi2) -> (lambda, local_sum[1] fp64)
     probs: Callable       # (lambda, total[1]) -> p
     sample: Callable      # (p, m, seed, row_base) -> (idx, weight, count[1])
+    probs_sample: Callable | None = None   # fused: (lambda, total[1], m, seed, row_base) -> (p, idx, weight, count)
 
 
 def cuda_ops() -> Ops:
@@ -61,7 +62,9 @@ def cuda_ops() -> Ops:
     return Ops(sketch=lambda A, sg, c, h, s, r1: api.fct_sketch(A, sg, c, h, s, r1),
                condition=_cond, rownorm=_rown,
                probs=lambda lam, tot: api.l1_probs(lam, tot),
-               sample=lambda p, m, seed, row_base: api.l1_sample(p, m, seed, row_base=row_base))
+               sample=lambda p, m, seed, row_base: api.l1_sample(p, m, seed, row_base=row_base),
+               probs_sample=lambda lam, tot, m, seed, row_base: api.l1_probs_sample(lam, tot, m, seed,
+                                                                                    row_base=row_base))
 
 
 @dataclass
@@ -97,8 +100,11 @@ def run_step(ops: Ops, shard: Shard, A, signs, cauchy, hash_rows, Pi2, s: int, r
     if shard.world > 1:
         dist.all_reduce(total, op=dist.ReduceOp.SUM, group=group)      # C3: one fp64 scalar
     mark("allreduce_sum")
-    p = ops.probs(lam, total)
-    idx, w, cnt = ops.sample(p, m, seed, shard.row0)
+    if ops.probs_sample is not None:
+        p, idx, w, cnt = ops.probs_sample(lam, total, m, seed, shard.row0)
+    else:
+        p = ops.probs(lam, total)
+        idx, w, cnt = ops.sample(p, m, seed, shard.row0)
     mark("sample")
     return StepResult(Y, R, Rinv, lam, p, total, idx, w, cnt, tuple(cond[2:]))
 

@@ -219,6 +219,32 @@ def test_sample_explicit_uniforms_and_capacity(fct):
     np.testing.assert_array_equal(a[0].numpy(), b[0].numpy())
 
 
+@pytest.mark.parametrize("n,m,row_base,cap", [(1, 1, 0, None), (2047, 100, 0, None), (2049, 100, 7, None),
+                                              (300001, 4096, 123456, None), (1 << 20, 65536, 1 << 30, None),
+                                              (50000, 3000, 5, 100)])
+def test_probs_sample_fused_bit_exact(fct, n, m, row_base, cap):
+    """Fused single-pass probabilities + sampling (decoupled look-back) == oracle probabilities and
+    sampler bit for bit; == the unfused l1_probs -> l1_sample path."""
+    rng = np.random.default_rng(n)
+    lam = np.abs(rng.standard_cauchy(n)).astype(np.float32)
+    lam[:2] = 0.0
+    tot = np.array([lam.astype(np.float64).sum()])
+    capacity = 2 * m + n // 10 + 64 if cap is None else cap
+    p, idx, w, cnt = fct.l1_probs_sample(dev(lam), dev(tot), m, seed=3, row_base=row_base, capacity=capacity)
+    p_o = (lam.astype(np.float64) / tot[0]).astype(np.float32)
+    np.testing.assert_array_equal(p.cpu().numpy(), p_o)
+    oi, ow, oc = oracle.sample(p_o, m, seed=3, row_base=row_base)
+    c = int(cnt.item())
+    assert c == oc
+    k = min(c, capacity)
+    np.testing.assert_array_equal(idx.cpu().numpy()[:k], oi[:k])
+    np.testing.assert_array_equal(w.cpu().numpy()[:k], ow[:k])
+    p2 = fct.l1_probs(dev(lam), dev(tot))
+    i2, w2, c2 = fct.l1_sample(p2, m, seed=3, row_base=row_base, capacity=capacity)
+    assert int(c2.item()) == c
+    np.testing.assert_array_equal(i2.cpu().numpy()[:k], idx.cpu().numpy()[:k])
+
+
 # ---------------------------------------------------------------- whole pipeline vs oracle pipeline
 @pytest.mark.parametrize("c", [1, 2])
 def test_pipeline_end_to_end(fct, c):
