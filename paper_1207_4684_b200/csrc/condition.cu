@@ -62,8 +62,8 @@ __global__ void __launch_bounds__(1024) chol_kernel(const double* __restrict__ G
                                                     const double* __restrict__ Rprev,
                                                     const double* __restrict__ Rprev_inv, double* Rk_out,
                                                     double* Rkinv_out, double* R, double* Rinv,
-                                                    int* __restrict__ info) {  // R/Rk_out may alias
-  extern __shared__ double G[];  // d x d
+                                                    int* __restrict__ info, int big) {  // R/Rk_out may alias
+  extern __shared__ double G[];  // d x d (+ 2 d x d when big)
   __shared__ int fail;
   const int tid = threadIdx.x, nt = blockDim.x;
   if (Rprev && *info != 0) return;  // first pass already failed: keep its info
@@ -101,38 +101,63 @@ __global__ void __launch_bounds__(1024) chol_kernel(const double* __restrict__ G
     if (tid == 0) *info = fail;
     return;
   }
-  // Rk (upper) -> Rk_out; Rk^-1 column c by thread c (back substitution), into Rkinv_out
-  for (int e = tid; e < d * d; e += nt) {
-    const int i = e / d, j = e - i * d;
-    Rk_out[e] = j >= i ? G[e] : 0.0;
-  }
+  // Rk^-1 by back substitution, column c by thread c, in shared memory when two more d x d arrays fit
+  // (X = Rk^-1, S = staging for the previous factor); otherwise in the global outputs
+  double* X = big ? G + d * d : Rkinv_out;
+  double* S = big ? G + 2 * d * d : nullptr;
   for (int c = tid; c < d; c += nt) {
     for (int i = d - 1; i >= 0; --i) {
       double v = 0.0;
       if (i <= c) {
         double s = (i == c) ? 1.0 : 0.0;
-        for (int l = i + 1; l <= c; ++l) s -= G[i * d + l] * Rkinv_out[l * d + c];
+        for (int l = i + 1; l <= c; ++l) s = fma(-G[i * d + l], X[l * d + c], s);
         v = s / G[i * d + i];
       }
-      Rkinv_out[i * d + c] = v;
+      X[i * d + c] = v;
     }
   }
   __syncthreads();
-  // combine with the previous factor
   for (int e = tid; e < d * d; e += nt) {
     const int i = e / d, j = e - i * d;
-    double r = 0.0, ri = 0.0;
-    if (j >= i) {
-      if (Rprev) {
-        for (int l = i; l <= j; ++l) r = fma(G[i * d + l], Rprev[l * d + j], r);
-        for (int l = i; l <= j; ++l) ri = fma(Rprev_inv[i * d + l], Rkinv_out[l * d + j], ri);
-      } else {
-        r = G[e];
-        ri = Rkinv_out[e];
-      }
+    Rk_out[e] = j >= i ? G[e] : 0.0;
+    if (big) Rkinv_out[e] = X[e];
+  }
+  // combine with the previous factor: R = Rk Rprev, R^-1 = Rprev^-1 Rk^-1 (all upper triangular)
+  if (Rprev) {
+    const double* P = Rprev;
+    if (big) {
+      for (int e = tid; e < d * d; e += nt) S[e] = Rprev[e];
+      __syncthreads();
+      P = S;
     }
-    R[e] = r;
-    Rinv[e] = ri;
+    for (int e = tid; e < d * d; e += nt) {
+      const int i = e / d, j = e - i * d;
+      double r = 0.0;
+      if (j >= i)
+        for (int l = i; l <= j; ++l) r = fma(G[i * d + l], P[l * d + j], r);
+      R[e] = r;
+    }
+    __syncthreads();
+    if (big) {
+      for (int e = tid; e < d * d; e += nt) S[e] = Rprev_inv[e];
+      __syncthreads();
+      P = S;
+    } else {
+      P = Rprev_inv;
+    }
+    for (int e = tid; e < d * d; e += nt) {
+      const int i = e / d, j = e - i * d;
+      double ri = 0.0;
+      if (j >= i)
+        for (int l = i; l <= j; ++l) ri = fma(P[i * d + l], X[l * d + j], ri);
+      Rinv[e] = ri;
+    }
+  } else {
+    for (int e = tid; e < d * d; e += nt) {
+      const int i = e / d, j = e - i * d;
+      R[e] = j >= i ? G[e] : 0.0;
+      Rinv[e] = X[e];
+    }
   }
   if (tid == 0) *info = 0;
 }
@@ -165,17 +190,18 @@ extern "C" fct_status fct_condition(const float* Y, int32_t r1, int64_t d, doubl
   double* R2inv = cv.take<double>((size_t)d * d);
   const int dd = (int)d;
   const int nt = (dd + kT - 1) / kT;
-  const size_t smem = sizeof(double) * (size_t)d * d;
+  const int big = 3 * sizeof(double) * (size_t)d * d <= 200 * 1024 ? 1 : 0;
+  const size_t smem = sizeof(double) * (size_t)d * d * (big ? 3 : 1);
   FCT_CUDA_RET(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   gram_kernel<float><<<dim3(nt, nt, nch), kT * 8, 0, st>>>(Y, r1, dd, Gp);
   FCT_LAUNCHED("gram_kernel<float>", st);
-  chol_kernel<<<1, 1024, smem, st>>>(Gp, nch, dd, nullptr, nullptr, R1, R1inv, R1, R1inv, info);
+  chol_kernel<<<1, 1024, smem, st>>>(Gp, nch, dd, nullptr, nullptr, R1, R1inv, R1, R1inv, info, big);
   FCT_LAUNCHED("chol_kernel(1)", st);
   apply_rinv_kernel<<<fct::num_sms() * 4, 256, 0, st>>>(Y, R1inv, r1, dd, Q);
   FCT_LAUNCHED("apply_rinv_kernel", st);
   gram_kernel<double><<<dim3(nt, nt, nch), kT * 8, 0, st>>>(Q, r1, dd, Gp);
   FCT_LAUNCHED("gram_kernel<double>", st);
-  chol_kernel<<<1, 1024, smem, st>>>(Gp, nch, dd, R1, R1inv, R2, R2inv, R, Rinv, info);
+  chol_kernel<<<1, 1024, smem, st>>>(Gp, nch, dd, R1, R1inv, R2, R2inv, R, Rinv, info, big);
   FCT_LAUNCHED("chol_kernel(2)", st);
   return FCT_OK;
 }
