@@ -178,7 +178,10 @@ extern "C" fct_status fct_sketch(const float* A, int64_t n, int64_t d, int64_t l
     FCT_CHECK_ARG(hb == 0, FCT_ERR_ARG, "fct_sketch: %d hash_rows entries outside [0, r1)", hb);
   }
   fct_status rc = FCT_ERR_UNSUPPORTED;
-  if (!getenv("FCT_SKETCH_GENERIC")) rc = fct_sketch_v1(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st);
+  if (!getenv("FCT_SKETCH_GENERIC")) {
+    rc = fct_sketch_v3(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st);
+    if (rc == FCT_ERR_UNSUPPORTED) rc = fct_sketch_v1(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st);
+  }
   if (rc == FCT_ERR_UNSUPPORTED) switch (dt) {
     case 32: rc = launch_generic<32>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
     case 16: rc = launch_generic<16>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
