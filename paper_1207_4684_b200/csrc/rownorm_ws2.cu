@@ -174,16 +174,46 @@ struct Smem {   // byte offsets inside the 1024-aligned dynamic shared memory
   int a, b, m64, cm, nrm, cq, bars, total;
 };
 constexpr int kCQ = 4;   // candidate-descriptor ring (selection -> recompute warps)
-__host__ __device__ inline Smem layout(int d, int KK, int NA, int ND) {
+// fp64 M for the exact candidate recompute: read through L1 from global memory (14 KB at d = 64, k = 27)
+// so that the shared memory holds one more 32 KB tile buffer (tiles stay until their rows are final)
+constexpr bool kM64Smem = true;
+
+// FCT_ROWNORM_DIAG bit 3 (diagnostics only): per-warp cycles spent in mbarrier waits and in total, CTA 0
+__device__ unsigned long long g_rn_prof[32][2];
+__device__ unsigned long long g_rn_cta[1024][2];   // per-CTA globaltimer at start / end (FCT_ROWNORM_PROF)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct WaitClock {
+  bool on;
+  unsigned long long waited = 0, t0 = 0;
+  __device__ explicit WaitClock(bool o) : on(o) { if (on) t0 = clock64(); }
+  template <class F>
+  __device__ __forceinline__ void wait(F f) {
+    if (!on) { f(); return; }
+    const unsigned long long a = clock64();
+    f();
+    waited += clock64() - a;
+  }
+  __device__ void flush(int warp) {
+    if (on && (threadIdx.x & 31) == 0 && blockIdx.x == 0) {
+      g_rn_prof[warp][0] = waited;
+      g_rn_prof[warp][1] = clock64() - t0;
+    }
+  }
+};
+__host__ __device__ inline Smem layout(int d, int KK, int NA, int ND, bool cq = true) {
   const int nch = (d + 31) / 32;
   Smem s;
   s.a = 0;
   s.b = s.a + NA * nch * 16384;          // B = [M_hi | M_lo]^T: nch chunks x 64 rows x 128 B
   s.m64 = s.b + nch * 8192;
-  s.cm = s.m64 + ((d * KK * 8 + 15) & ~15);
+  s.cm = s.m64 + (kM64Smem ? ((d * KK * 8 + 15) & ~15) : 0);
   s.nrm = s.cm + 32 * 4;
   s.cq = s.nrm + ND * 128 * 4;           // [kCQ][128] descriptors + [kCQ][128] settled lambdas
-  s.bars = s.cq + kCQ * 128 * 8;
+  s.bars = s.cq + (cq ? kCQ * 128 * 8 : 0);
   s.total = s.bars + 8 * (2 * NA + 4 + 3 * ND + 2 * kCQ);
   return s;
 }
@@ -197,16 +227,16 @@ __global__ void __launch_bounds__(32 * (kEpiWarp0 + 4 * EG + 4 * RG), 1)
 rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ A, int64_t n, int d, int64_t lda,
                    const float* __restrict__ M32g, int KP32, const double* __restrict__ M64g,
                    const float* __restrict__ colbg, float gam, int NA, int ND, float* __restrict__ lambda,
-                   double* __restrict__ partial, int diag) {
+                   double* __restrict__ partial, int diag, unsigned whint) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* base = smraw + ((1024u - (tcx::su32(smraw) & 1023u)) & 1023u);
   const int dd = D ? D : d;
   const int nch = (dd + 31) >> 5, KP = nch * 32;
   const int tile_floats = nch * 128 * 32;
-  const Smem L = layout(dd, KK, NA, ND);
+  const Smem L = layout(dd, KK, NA, ND, RG > 0);
   float* sA = (float*)(base + L.a);
   float* sB = (float*)(base + L.b);
-  double* M64 = (double*)(base + L.m64);
+  const double* M64 = kM64Smem ? (const double*)(base + L.m64) : M64g;
   float* cm = (float*)(base + L.cm);
   float* norms = (float*)(base + L.nrm);
   uint64_t* tma_full = (uint64_t*)(base + L.bars);   // [NA]  tile landed
@@ -257,7 +287,8 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
     const float hi = tcx::trunc_tf32(m);
     sB[(l >> 5) * 64 * 32 + jj * 32 + ((((l & 31) >> 2) ^ (jj & 7)) << 2) + (l & 3)] = jj < 32 ? hi : m - hi;
   }
-  for (int e = tid; e < KK * dd; e += blockDim.x) M64[e] = M64g[e];
+  if (kM64Smem)
+    for (int e = tid; e < KK * dd; e += blockDim.x) ((double*)(base + L.m64))[e] = M64g[e];
   for (int e = tid; e < 32; e += blockDim.x) cm[e] = e < KK ? colbg[2 * e] : 0.f;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -266,6 +297,10 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
   const uint32_t tm = tbase;
   const int acols = abuf_cols<AT>(KP);
   const uint32_t dcol0 = 2u * acols;   // TMEM: [A buf 0][A buf 1][D 0] ... [D ND-1], D = 64 columns
+  const bool prof = (diag & 8) != 0;
+  diag &= 7;
+  WaitClock wc(prof);
+  if (prof && threadIdx.x == 0) g_rn_cta[blockIdx.x][0] = gtimer();
   const int ntiles = (int)((n + 127) / 128);
   const int t0 = blockIdx.x, tstep = gridDim.x;
   const int my_tiles = t0 < ntiles ? (ntiles - 1 - t0) / tstep + 1 : 0;
@@ -278,8 +313,8 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
     unsigned pa = 0, pd = 0;   // phase parities of the current ring slots
     for (int i = 0; i < my_tiles; ++i) {
       const int sl = i & 1;
-      tcx::bar_wait(&tma_full[sa], pa);
-      if (i >= 2) tcx::bar_wait(&at_free[sl], (unsigned)(((i - 2) >> 1) & 1));
+      wc.wait([&] { tcx::bar_wait(&tma_full[sa], pa); });
+      if (i >= 2) wc.wait([&] { tcx::bar_wait(&at_free[sl], (unsigned)(((i - 2) >> 1) & 1)); });
       const float* tile = sA + sa * tile_floats;
       const uint32_t tb = tm + lane_off + (uint32_t)(sl * acols);
       float s2 = 0.f, s2b = 0.f;
@@ -311,7 +346,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) tcx::bar_arrive(&at_full[sl]);
-      if (i >= ND) tcx::bar_wait(&d_free[sd], pd ^ 1u);
+      if (i >= ND) wc.wait([&] { tcx::bar_wait(&d_free[sd], pd ^ 1u); });
       norms[sd * 128 + tid] = s2 + s2b;
       __syncwarp();
       if (lane == 0) tcx::bar_arrive(&n_full[sd]);
@@ -324,7 +359,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
       int sa = 0;
       unsigned pa = 0;
       for (int j = 0; j < my_tiles; ++j) {
-        if (j >= NA) tcx::bar_wait(&a_free[sa], pa ^ 1u);
+        if (j >= NA) wc.wait([&] { tcx::bar_wait(&a_free[sa], pa ^ 1u); });
         tcx::tma_tile(sA + sa * tile_floats, &tmA, nch, (t0 + j * tstep) * 128, &tma_full[sa]);
         if (++sa == NA) { sa = 0; pa ^= 1u; }
       }
@@ -340,8 +375,8 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
       unsigned pd = 0;
       for (int i = 0; i < my_tiles; ++i) {
         const int sl = i & 1;
-        tcx::bar_wait(&at_full[sl], (unsigned)((i >> 1) & 1));   // implies the TMA tile has landed
-        if (i >= ND) tcx::bar_wait(&d_free[sd], pd ^ 1u);
+        wc.wait([&] { tcx::bar_wait(&at_full[sl], (unsigned)((i >> 1) & 1)); });   // implies the TMA tile has landed
+        if (i >= ND) wc.wait([&] { tcx::bar_wait(&d_free[sd], pd ^ 1u); });
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t tD = tm + dcol0 + (uint32_t)(sd * 64);
         const uint32_t tA = tm + (uint32_t)(sl * acols);
@@ -379,8 +414,10 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
     int sd = g % ND, sa = g % NA, cs = g % kCQ;
     unsigned ph = (unsigned)((g / ND) & 1), pc = (unsigned)((g / kCQ) & 1);
     for (int i = g; i < my_tiles; i += EG) {
-      tcx::bar_wait(&d_full[sd], ph);
-      tcx::bar_wait(&n_full[sd], ph);
+      wc.wait([&] {
+        tcx::bar_wait_sleep(&d_full[sd], ph, whint);
+        tcx::bar_wait_sleep(&n_full[sd], ph, whint);
+      });
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       uint32_t dv[32];
       {
@@ -435,7 +472,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
     int sa = g % NA, cs = g % kCQ;
     unsigned pc = (unsigned)((g / kCQ) & 1);
     for (int i = g; i < my_tiles; i += RG) {
-      tcx::bar_wait(&c_full[cs], pc);
+      tcx::bar_wait_sleep(&c_full[cs], pc, whint);
       const uint32_t desc = cdesc[cs * 128 + r];
       float lam = clam[cs * 128 + r];
       __syncwarp();
@@ -456,6 +493,8 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
       while (cs >= kCQ) { cs -= kCQ; pc ^= 1u; }
     }
   }
+  wc.flush(warp);
+  if (prof && threadIdx.x == 0) g_rn_cta[blockIdx.x][1] = gtimer();
   for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
   if (lane == 0) red[warp] = local;
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -497,16 +536,17 @@ fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M3
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   FCT_CHECK_ARG(cr == CUDA_SUCCESS, FCT_ERR_CUDA, "l1_rownorm: cuTensorMapEncodeTiled failed (%d)", (int)cr);
   const int nch = (d + 31) / 32, KP = nch * 32;
-  const bool at = 4 * KP + 4 * 64 <= 512 && !getenv("FCT_ROWNORM_ASS");   // A_hi from TMEM when it fits
+  // A_hi from TMEM when it fits next to EG + 1 accumulators (else from shared memory, SS form)
+  const bool at = 4 * KP + 64 * (EG + 1) <= 512 && !getenv("FCT_ROWNORM_ASS");
   const int ND = std::min(8, (512 - 2 * (at ? 2 * KP : KP)) / 64);
   int NA = 0;
   for (int na = 8; na >= 2; --na)
-    if (layout(d, KK, na, ND).total + 1024 <= (int)kSmemMax - 2048) { NA = na; break; }
+    if (layout(d, KK, na, ND, RG > 0).total + 1024 <= (int)kSmemMax - 2048) { NA = na; break; }
   if (NA < 2 || ND < EG + 1) return FCT_ERR_UNSUPPORTED;
   // keep the tile until the epilogue is done (exact recompute from shared memory) when enough buffers fit
   const bool keep = NA >= EG + 2 && !getenv("FCT_ROWNORM_NOKEEP");
   if (RG > 0 && !keep) return FCT_ERR_UNSUPPORTED;
-  const size_t smem = (size_t)layout(d, KK, NA, ND).total + 1024;
+  const size_t smem = (size_t)layout(d, KK, NA, ND, RG > 0).total + 1024;
   const int g = std::max(1, std::min(grid, fct::num_sms()));
   const int threads = 32 * (kEpiWarp0 + 4 * EG + 4 * RG);
   const float gam = 6.103515625e-05f * 1.05f;   // 3xTF32 bound, 2^-14 (measured 1.9e-6) x 1.05 for roundings
@@ -518,8 +558,32 @@ fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M3
             RG, (int)keep, (int)at, g, NA, ND, smem);
   FCT_CUDA_RET(cudaMemsetAsync(partial, 0, sizeof(double) * grid, st));
   const char* dg = getenv("FCT_ROWNORM_DIAG");
-  kern<<<g, threads, smem, st>>>(map, A, n, d, lda, M32, KP32, M64, colb, gam, NA, ND, lambda, partial, dg ? atoi(dg) : 0);
+  const int diag = dg ? atoi(dg) : 0;
+  const char* wh = getenv("FCT_WAIT_HINT");
+  kern<<<g, threads, smem, st>>>(map, A, n, d, lda, M32, KP32, M64, colb, gam, NA, ND, lambda, partial, diag,
+                                 wh ? (unsigned)atoi(wh) : 20000u);
   FCT_LAUNCHED("rownorm_ws2_kernel", st);
+  if (diag & 8) {
+    unsigned long long h[32][2];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_rn_prof, sizeof(h));
+    unsigned long long c[1024][2];
+    cudaMemcpyFromSymbol(c, g_rn_cta, sizeof(c));
+    unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
+    for (int b = 0; b < g; ++b) {
+      s0 = std::min(s0, c[b][0]); s1 = std::max(s1, c[b][0]);
+      e0 = std::min(e0, c[b][1]); e1 = std::max(e1, c[b][1]);
+    }
+    fprintf(stderr, "[fct prof] %d CTAs: start spread %.1f us, first end %.1f us, last end %.1f us\n", g,
+            (s1 - s0) * 1e-3, (e0 - s0) * 1e-3, (e1 - s0) * 1e-3);
+    for (int b = 0; b < g; b += 16)
+      fprintf(stderr, "[fct prof] cta %3d start %8.1f end %8.1f us\n", b, (c[b][0] - s0) * 1e-3, (c[b][1] - s0) * 1e-3);
+    const int nw = threads / 32;
+    for (int w = 0; w < nw; ++w)
+      fprintf(stderr, "[fct prof] warp %2d %-9s waited %5.1f%% of %llu cycles\n", w,
+              w < 4 ? "split" : w == 4 ? "tma" : w == 5 ? "mma" : (w < kEpiWarp0 + 4 * EG ? "epilogue" : "recompute"),
+              100.0 * h[w][0] / (double)(h[w][1] ? h[w][1] : 1), h[w][1]);
+  }
   return FCT_OK;
 }
 
@@ -536,6 +600,10 @@ fct_status launch_k(const float* A, int64_t n, int d, int64_t lda, const float* 
     if (var == 0) rc_ = launch<KK, DD, 2, 2>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st); \
     if (rc_ != FCT_ERR_UNSUPPORTED) return rc_;                                                            \
     if (var == 2) return launch<KK, DD, 2, 0>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st); \
+    if (var == 3) {                                                                                        \
+      rc_ = launch<KK, DD, 4, 0>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st);           \
+      if (rc_ != FCT_ERR_UNSUPPORTED) return rc_;                                                          \
+    }                                                                                                      \
     return launch<KK, DD, 3, 0>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st);            \
   } while (0)
   if (d == DC) FCT_RN_LAUNCH(DC);

@@ -21,23 +21,25 @@ __device__ __forceinline__ void bar_init(uint64_t* b, unsigned cnt) {
 __device__ __forceinline__ void bar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
 }
-// blocking wait on the phase with parity `ph` (FCT_WAIT_HINT: optional suspend-time hint in ns)
+// blocking wait on the phase with parity `ph`
 __device__ __forceinline__ void bar_wait(uint64_t* b, unsigned ph) {
-#ifdef FCT_WAIT_HINT
-  asm volatile(
-      "{\n.reg .pred p;\nBW_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra BW_%=;\n}\n" ::"r"(su32(b)),
-      "r"(ph), "r"((unsigned)FCT_WAIT_HINT)
-      : "memory");
-#else
   asm volatile(
       "{\n.reg .pred p;\nBW_%=:\n"
       "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra BW_%=;\n}\n" ::"r"(su32(b)),
       "r"(ph)
       : "memory");
-#endif
+}
+// the same for warps that may wait long (consumers of a slower stage): the suspend-time hint lets the
+// hardware park the warp until the phase completes instead of re-issuing try_wait, which would steal
+// issue slots from the producer warps sharing the SM sub-partition
+__device__ __forceinline__ void bar_wait_sleep(uint64_t* b, unsigned ph, unsigned hint_ns) {
+  asm volatile(
+      "{\n.reg .pred p;\nBS_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra BS_%=;\n}\n" ::"r"(su32(b)),
+      "r"(ph), "r"(hint_ns)
+      : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b)) : "memory");
