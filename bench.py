@@ -38,6 +38,23 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def load_traffic(cfg, n_loc, world):
+    """DRAM bytes per launch (read + write) of each kernel from the committed ncu --set full capture of this
+    exact workload (profiles/r01_ncu_full_cfg4_traffic.json); {} when the capture does not match."""
+    p = os.path.join(ROOT, "profiles", "r01_ncu_full_cfg4_traffic.json")
+    try:
+        with open(p) as f:
+            m = json.load(f)
+        w = m["workload"]
+        if world != 1 or cfg.idx != w["config"] or n_loc != w["n"] or cfg.d != w["d"]:
+            return {}
+        out = {k: v["dram_bytes_read"] + v["dram_bytes_write"] for k, v in m["kernels"].items()}
+        out["_source"] = "profiles/r01_ncu_full_cfg4_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum)"
+        return out
+    except Exception:
+        return {}
+
+
 def workload_desc(cfg, n_total):
     kinds = {1: "i.i.d. N(0,1)", 2: "N(0,1) features + planted l1 regression column -b",
              3: "N(0,1) rows x min(|Cauchy|^0.5, 1e4)", 4: "N(0,1), 1% of rows x1e3",
@@ -182,7 +199,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-blocks", type=int, default=256)
+    ap.add_argument("--cpu-blocks", type=int, default=2560)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -266,12 +283,15 @@ def main():
     t_rn = stage_ms["rownorm"]["mean"] * 1e-3
     kern = {"fct1_sketch": (sk_bytes, t_sk), "l1_rownorm": (rn_bytes, t_rn)}
     dom = max(kern, key=lambda k: kern[k][1])
+    traffic = load_traffic(cfg, n_loc, world)
     rl = {}
     for kname, (byt, t) in kern.items():
         ach = byt / t / 1e9
         rl[kname] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                     "traffic": None, "algorithmic_bytes_per_launch": byt, "ms_per_launch": t * 1e3,
+                     "traffic": traffic.get(kname), "algorithmic_bytes_per_launch": byt, "ms_per_launch": t * 1e3,
                      "frac_of_8TBs": ach / 8000.0}
+        if traffic.get(kname):
+            rl[kname]["traffic_source"] = traffic["_source"]
     roofline = dict(rl[dom])
     roofline["kernel"] = dom
     roofline["peak_source"] = peak_src
