@@ -105,6 +105,20 @@ size_t l1_rownorm_workspace_bytes(int64_t n, int64_t d, int32_t k);
 fct_status l1_rownorm(const float* A, int64_t n, int64_t d, int64_t lda, const double* Rinv,
                       const float* Pi2, int32_t k, float* lambda, double* lambda_sum,
                       void* workspace, size_t workspace_bytes, void* stream);
+/* NEXT-1: exact l1 row norms of the well-conditioned basis U = A R^-1,
+ *     lambda[i] = sum_j |sum_l A[i][l] Rinv[l][j]|      (Sec. 6.2: the paper's
+ * experiments "compute the row norms of U exactly instead of estimating them"; U of FastL1Basis
+ * P:L2771-2796).  *lambda_sum = sum_i lambda[i] (fp64, overwritten).  A: n x d fp32 row-major (lda),
+ * Rinv: d x d fp64 row-major (device).  The contraction runs on the tensor cores with every product of
+ * two-term fp32 splits formed; accuracy: |lambda - exact| <= 2^-14 sum_j sum_l |A_il||Rinv_lj| + 2^-17
+ * lambda.  d <= 64 with d % 4 == 0, lda % 4 == 0, 16-byte aligned A and n < 2^31 takes the
+ * tensor-core kernel; other shapes (d <= FCT_MAX_D) a SIMT fp32 kernel with the same tolerance.
+ * workspace: l1_rownorm_exact_workspace_bytes(n, d) device bytes.
+ */
+size_t l1_rownorm_exact_workspace_bytes(int64_t n, int64_t d);
+fct_status l1_rownorm_exact(const float* A, int64_t n, int64_t d, int64_t lda, const double* Rinv,
+                            float* lambda, double* lambda_sum, void* workspace,
+                            size_t workspace_bytes, void* stream);
 /* p[i] = (float)((double)lambda[i] / *lambda_total)   (t_i of P:L2028-2033). */
 fct_status l1_probs(const float* lambda, int64_t n, const double* lambda_total, float* p,
                     void* stream);

@@ -7,6 +7,7 @@ import this package.  It shares no code with paper_1207_4684_b200 (the CUDA path
   dense_sketch    O1-dense: materialised B, C, H~, D (numpy, tiny n)             -> dense.py
   condition(Y)    O2  Householder QR of Y = Pi1 A, diag(R) > 0, R^-1
   rownorm(...)    O3  lambda_i = median_j |(A R^-1 Pi2)_ij|   P:L2921-2938        -> oracle.c
+  rownorm_exact   NEXT-1  lambda_i = ||(A R^-1)_i||_1 (exact row norms) -> oracle.c
   probs(...)          p_i = lambda_i / sum lambda   (t_i of P:L2028-2033)
   sample(...)     O4  Bernoulli l1 sampling   P:L1258-1268                        -> oracle.c
 Parity-unpinned items are listed in DESIGN.md ("Oracle pins").
@@ -44,6 +45,8 @@ def _L():
         lib.or_sketch.argtypes = [vp, i64, i64, i64, vp, vp, vp, i32, i32, i64, i64, vp, vp]
         lib.or_rownorm.restype = ctypes.c_int
         lib.or_rownorm.argtypes = [vp, i64, i64, i64, vp, vp, i32, vp, vp, vp]
+        lib.or_rownorm_exact.restype = ctypes.c_int
+        lib.or_rownorm_exact.argtypes = [vp, i64, i64, i64, vp, vp, vp, vp]
         lib.or_sample.restype = i64
         lib.or_sample.argtypes = [vp, vp, i64, i64, i64, u64, vp, vp, i64]
         _lib = lib
@@ -111,6 +114,21 @@ def rownorm(A: np.ndarray, Rinv: np.ndarray, Pi2: np.ndarray, with_bound: bool =
     rc = _L().or_rownorm(_p(A), n, d, d, _p(Rinv), _p(Pi2), k, _p(lam), _p(tot), _p(bnd))
     if rc != 0:
         raise ValueError("or_rownorm failed")
+    return (lam, float(tot[0]), bnd) if with_bound else (lam, float(tot[0]))
+
+
+def rownorm_exact(A: np.ndarray, Rinv: np.ndarray, with_bound: bool = False):
+    """NEXT-1: exact l1 row norms lambda_i = ||(A R^-1)_i||_1 (fp64), sum, [bound_i = sum_j sum_l |A_il||Rinv_lj|]
+    -- the row norms the paper's Sec. 6.2 experiments compute exactly."""
+    A = np.ascontiguousarray(A, np.float32)
+    n, d = A.shape
+    Rinv = np.ascontiguousarray(Rinv, np.float64)
+    lam = np.empty(n, np.float64)
+    tot = np.zeros(1, np.float64)
+    bnd = np.empty(n, np.float64) if with_bound else None
+    rc = _L().or_rownorm_exact(_p(A), n, d, d, _p(Rinv), _p(lam), _p(tot), _p(bnd))
+    if rc != 0:
+        raise ValueError("or_rownorm_exact failed")
     return (lam, float(tot[0]), bnd) if with_bound else (lam, float(tot[0]))
 
 

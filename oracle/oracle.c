@@ -11,6 +11,7 @@
  *                matrix of P:L2273-2284; H~ = blockdiag([H_s; I_s]) P:L2246-2266;
  *                D = Rademacher signs, the north_star addition, reading R1)
  *   or_rownorm  lambda_i = median_j |(A R^-1 Pi2)_ij|, with R^-1 Pi2 formed first
+ *   or_rownorm_exact  lambda_i = ||(A R^-1)_i||_1 (the exact row norms of Sec. 6.2)
  *               P:L2921-2938
  *   or_sample   phat_i = min(1, m p_i), keep i w.p. phat_i, weight 1/phat_i
  *               l1 sampling lemma P:L1258-1268, use P:L2028-2033
@@ -175,6 +176,34 @@ int or_rownorm(const float* A, int64_t n, int64_t d, int64_t lda, const double* 
     free(v);
   }
   free(M);
+  if (lambda_sum) *lambda_sum = total;
+  return 0;
+}
+
+/*
+ * Exact l1 row norms of U = A R^-1 ("we compute the row norms of U exactly instead
+ * of estimating them"; U of FastL1Basis P:L2771-2796):  lambda_i = sum_j |sum_l A_il Rinv_lj|  (fp64).
+ * bound (optional): bound_i = sum_j sum_l |A_il| |Rinv_lj|  (magnitude of the dot products).
+ */
+int or_rownorm_exact(const float* A, int64_t n, int64_t d, int64_t lda, const double* Rinv, double* lambda,
+                     double* lambda_sum, double* bound) {
+  if (n < 0 || d < 1 || lda < d) return -1;
+  double total = 0.0;
+#pragma omp parallel for schedule(static) reduction(+ : total)
+  for (int64_t i = 0; i < n; ++i) {
+    double lam = 0.0, mag = 0.0;
+    for (int64_t j = 0; j < d; ++j) {
+      double u = 0.0;
+      for (int64_t l = 0; l < d; ++l) {
+        u += (double)A[i * lda + l] * Rinv[l * d + j];
+        mag += fabs((double)A[i * lda + l]) * fabs(Rinv[l * d + j]);
+      }
+      lam += fabs(u);
+    }
+    lambda[i] = lam;
+    if (bound) bound[i] = mag;
+    total += lam;
+  }
   if (lambda_sum) *lambda_sum = total;
   return 0;
 }

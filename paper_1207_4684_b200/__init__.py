@@ -13,6 +13,7 @@ from .api import (  # noqa: F401
     l1_probs,
     l1_probs_sample,
     l1_rownorm,
+    l1_rownorm_exact,
     l1_rownorm_probs,
     l1_sample,
     l1_sample_u,

@@ -22,6 +22,8 @@ SIGNATURES = {
     "fct_condition": (_int, [_vp, _i32, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "l1_rownorm_workspace_bytes": (_sz, [_i64, _i64, _i32]),
     "l1_rownorm": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "l1_rownorm_exact_workspace_bytes": (_sz, [_i64, _i64]),
+    "l1_rownorm_exact": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "l1_probs": (_int, [_vp, _i64, _vp, _vp, _vp]),
     "l1_rownorm_probs": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "l1_sample_workspace_bytes": (_sz, [_i64]),

@@ -113,6 +113,22 @@ def l1_rownorm(A, Rinv, Pi2, lam=None, lambda_sum=None):
     return lam, lambda_sum
 
 
+def l1_rownorm_exact(A, Rinv, lam=None, lambda_sum=None):
+    """NEXT-1: exact l1 row norms lambda_i = ||(A Rinv)_i||_1 (fp32) and their fp64 sum."""
+    L = _lib_()
+    if A.dtype != torch.float32 or not A.is_cuda or A.dim() != 2 or A.stride(1) != 1:
+        raise ValueError("A must be a 2-D fp32 CUDA tensor with unit column stride")
+    _need(Rinv, torch.float64, "Rinv")
+    n, d = A.shape
+    lam = torch.empty(n, dtype=torch.float32, device=A.device) if lam is None else lam
+    lambda_sum = torch.zeros(1, dtype=torch.float64, device=A.device) if lambda_sum is None else lambda_sum
+    nb = L.l1_rownorm_exact_workspace_bytes(n, d)
+    ws = workspace(nb, "rownorm_exact")
+    _lib.check(L.l1_rownorm_exact(_ptr(A), n, d, A.stride(0), _ptr(Rinv), _ptr(lam), _ptr(lambda_sum), _ptr(ws),
+                                  ws.numel(), _stream()))
+    return lam, lambda_sum
+
+
 def l1_probs(lam, lambda_total, p=None):
     L = _lib_()
     _need(lam, torch.float32, "lambda")

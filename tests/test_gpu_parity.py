@@ -371,3 +371,51 @@ def test_sketch_hot_buckets(fct, c, v3, monkeypatch):
     inp.hash = hot
     Yo2, Mb2 = oracle.sketch(inp.A, inp.signs, inp.cauchy, inp.hash, cfg.s, cfg.r1)
     assert_sketch_close(sketch_gpu(fct, inp), Yo2, Mb2)
+
+
+# ---------------------------------------------------------------- NEXT-1: exact l1 row norms (tcgen05)
+@pytest.mark.parametrize("c", [1, 2, 3, 4, 5])
+def test_rownorm_exact_configs(fct, c):
+    """lambda_i = ||(A R^-1)_i||_1 on the tensor cores vs the fp64 oracle, with R^-1 from the oracle's own
+    conditioning of the config's sketch.  Tolerance (derived from the arithmetic): 2^-14 times
+    the magnitude sum_j sum_l |A_il||R^-1_lj| plus 2^-17 relative (fp32 sum over j).  Both the stacked
+    (d <= 64) and the four-pass (d = 100) forms are covered; zero, tiny and huge rows included."""
+    cfg = fctgen.CONFIGS[c]
+    inp = fctgen.make_inputs(cfg, n=2 * cfg.s)
+    Rinv = _rinv_for(inp)
+    B = fctgen.matrix(cfg.kind, cfg.seed, max(cfg.n, 9000), cfg.d, 0, 9000 + 45)
+    B[0] = 0.0
+    B[1] *= np.float32(1e-20)
+    B[2] *= np.float32(1e15)
+    lam_o, tot_o, bnd = oracle.rownorm_exact(B, Rinv, with_bound=True)
+    lam, tot = fct.l1_rownorm_exact(dev(B), dev(Rinv))
+    lam = lam.cpu().numpy().astype(np.float64)
+    err = np.abs(lam - lam_o)
+    assert lam[0] == 0.0
+    assert (err <= 2.0 ** -14 * bnd + 2.0 ** -17 * lam_o).all(), f"max err/bound {np.max(err / np.maximum(bnd, 1e-300)):.3e}"
+    np.testing.assert_allclose(float(tot.item()), lam.sum(), rtol=1e-12)
+    # how many rows also meet the pure 1e-5 relative bar (reported, not required)
+    frac = float(np.mean(err <= 1e-5 * lam_o))
+    assert frac > 0.5
+
+
+def test_rownorm_exact_identity_and_errors(fct):
+    rng = np.random.default_rng(4)
+    A = rng.standard_normal((1000, 16)).astype(np.float32)
+    lam, _ = fct.l1_rownorm_exact(dev(A), dev(np.eye(16)))
+    np.testing.assert_allclose(lam.cpu().numpy(), np.abs(A.astype(np.float64)).sum(1), rtol=2e-6)
+    # d % 4 != 0 and the SIMT form (also forced for d = 16) agree with the oracle too
+    rng2 = np.random.default_rng(5)
+    for dd, force in ((10, False), (16, True)):
+        Rinv = np.triu(rng2.standard_normal((dd, dd))) + 2 * np.eye(dd)
+        B = A[:, :dd].copy()
+        lam_o, _, bnd = oracle.rownorm_exact(B, Rinv, with_bound=True)
+        import os
+        if force:
+            os.environ["FCT_ROWNORM_SIMT"] = "1"
+        try:
+            lam, _ = fct.l1_rownorm_exact(dev(B), dev(Rinv))
+        finally:
+            os.environ.pop("FCT_ROWNORM_SIMT", None)
+        err = np.abs(lam.cpu().numpy().astype(np.float64) - lam_o)
+        assert (err <= 2.0 ** -14 * bnd + 2.0 ** -17 * lam_o).all()

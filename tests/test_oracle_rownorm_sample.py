@@ -166,3 +166,50 @@ def test_sample_tie_rule_is_strict():
     u_below = np.nextafter(phat, 0.0)
     assert oracle.sample(p, m, u=u_eq)[2] == 0
     np.testing.assert_array_equal(oracle.sample(p, m, u=u_below)[0], np.arange(n))
+
+
+# ---------------------------------------------------------------- NEXT-1: exact l1 row norms of U = A R^-1
+def test_rownorm_exact_closed_forms():
+    """lambda_i = ||(A R^-1)_i||_1.  Closed forms that catch a transposed R^-1, a dropped
+    absolute value or a wrong index: Rinv = I -> ||a_i||_1; Rinv = diag(r) -> sum_l |a_il r_l|; a signed
+    permutation -> ||a_i||_1; A = e_l rows -> the l1 norm of ROW l of Rinv (not column l); d = 1 -> |a r|."""
+    rng = np.random.default_rng(11)
+    n, d = 300, 7
+    A = rng.standard_normal((n, d)).astype(np.float32)
+    A64 = A.astype(np.float64)
+    lam, tot = oracle.rownorm_exact(A, np.eye(d))
+    np.testing.assert_allclose(lam, np.abs(A64).sum(1), rtol=1e-15)
+    assert math.isclose(tot, float(np.abs(A64).sum()), rel_tol=1e-12)
+    r = rng.standard_normal(d) * 3
+    lam, _ = oracle.rownorm_exact(A, np.diag(r))
+    np.testing.assert_allclose(lam, np.abs(A64 * r).sum(1), rtol=1e-14)
+    P = np.eye(d)[rng.permutation(d)] * rng.choice([-1.0, 1.0], d)
+    lam, _ = oracle.rownorm_exact(A, P)
+    np.testing.assert_allclose(lam, np.abs(A64).sum(1), rtol=1e-14)
+    Rinv = np.triu(rng.standard_normal((d, d))) + 2 * np.eye(d)
+    E = np.eye(d, dtype=np.float32)
+    lam, _ = oracle.rownorm_exact(E, Rinv)
+    want = [math.fsum(abs(x) for x in Rinv[l, :]) for l in range(d)]
+    np.testing.assert_allclose(lam, want, rtol=1e-15)
+    assert not np.allclose(lam, np.abs(Rinv).sum(0))            # the column sums differ: orientation is pinned
+    lam, _ = oracle.rownorm_exact(A[:, :1].copy(), np.array([[-2.5]]))
+    np.testing.assert_allclose(lam, 2.5 * np.abs(A64[:, 0]), rtol=1e-15)
+
+
+def test_rownorm_exact_invariants_and_bound():
+    rng = np.random.default_rng(12)
+    n, d = 256, 6
+    A = rng.standard_normal((n, d)).astype(np.float32)
+    A[3] = 0.0
+    Rinv = np.triu(rng.standard_normal((d, d))) + 2 * np.eye(d)
+    lam, tot, bnd = oracle.rownorm_exact(A, Rinv, with_bound=True)
+    assert lam[3] == 0.0 and bnd[3] == 0.0
+    lam2, _ = oracle.rownorm_exact(A * np.float32(-8.0), Rinv)
+    np.testing.assert_allclose(lam2, 8.0 * lam, rtol=1e-14)          # |alpha| homogeneity
+    lam3, _ = oracle.rownorm_exact(A, 0.5 * Rinv)
+    np.testing.assert_allclose(lam3, 0.5 * lam, rtol=1e-14)
+    assert (lam <= bnd * (1 + 1e-12)).all()                            # triangle inequality
+    # brute force with exactly rounded sums on a few rows
+    for i in (0, 1, 100):
+        want = math.fsum(abs(math.fsum(float(A[i, l]) * Rinv[l, j] for l in range(d))) for j in range(d))
+        assert math.isclose(lam[i], want, rel_tol=1e-14)
