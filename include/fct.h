@@ -150,6 +150,21 @@ fct_status l1_sample_u(const float* p, const double* u, int64_t n, int64_t row_b
                        int64_t m, int64_t* idx, double* weight, int64_t capacity,
                        int64_t* count, void* workspace, size_t workspace_bytes, void* stream);
 
+/* NEXT-4: multinomial sampling -- exactly m i.i.d. row draws with probability
+ * proportional to p (the "sample m rows with probabilities p_i" reading of P:L1258-1268 / P:L2178-2188,
+ * drawn with replacement), from an exact fixed-point CDF so that the result is bit-exact:
+ *   F = 62 - ceil(log2 n) - e with max_i p_i < 2^e;  W_i = floor(p_i 2^F) (uint64; p_i <= 0 or NaN -> 0);
+ *   CDF_i = sum_{t<=i} W_t;  T = CDF_{n-1} (< 2^62)  -> *total (device uint64; 0: no positive p,
+ *   then idx[] = -1, weight[] = 0);  X_j = rng_u64(seed, 10, j) >> 11;  target_j = (X_j T) >> 53;
+ *   idx[j] = row_base + min{i : CDF_i > target_j};  weight[j] = (double)T / ((double)m (double)W_idx)
+ *   (= 1/(m phat_i), the Horvitz-Thompson weight).  idx/weight: m entries each (device).
+ * workspace: l1_sample_multinomial_workspace_bytes(n) device bytes.
+ */
+size_t l1_sample_multinomial_workspace_bytes(int64_t n);
+fct_status l1_sample_multinomial(const float* p, int64_t n, int64_t m, uint64_t seed, int64_t row_base,
+                                 int64_t* idx, double* weight, uint64_t* total, void* workspace,
+                                 size_t workspace_bytes, void* stream);
+
 /* Fused a9 + a10 (what the pipeline runs): p[i] = (float)((double)lambda[i] / *lambda_total)
  * exactly as l1_probs, then the Bernoulli sampling of l1_sample on that p, in ONE pass over
  * lambda (single-pass decoupled look-back compaction).  Outputs (p, idx, weight, count) are

@@ -10,6 +10,7 @@ import this package.  It shares no code with paper_1207_4684_b200 (the CUDA path
   rownorm_exact   NEXT-1  lambda_i = ||(A R^-1)_i||_1 (exact row norms) -> oracle.c
   probs(...)          p_i = lambda_i / sum lambda   (t_i of P:L2028-2033)
   sample(...)     O4  Bernoulli l1 sampling   P:L1258-1268                        -> oracle.c
+  sample_multinomial  NEXT-4  m i.i.d. draws from an exact fixed-point CDF          -> oracle.c
 Parity-unpinned items are listed in DESIGN.md ("Oracle pins").
 """
 from __future__ import annotations
@@ -47,6 +48,8 @@ def _L():
         lib.or_rownorm.argtypes = [vp, i64, i64, i64, vp, vp, i32, vp, vp, vp]
         lib.or_rownorm_exact.restype = ctypes.c_int
         lib.or_rownorm_exact.argtypes = [vp, i64, i64, i64, vp, vp, vp, vp]
+        lib.or_sample_multinomial.restype = u64
+        lib.or_sample_multinomial.argtypes = [vp, i64, i64, u64, i64, vp, vp, vp]
         lib.or_sample.restype = i64
         lib.or_sample.argtypes = [vp, vp, i64, i64, i64, u64, vp, vp, i64]
         _lib = lib
@@ -153,3 +156,17 @@ def sample(p32: np.ndarray, m: int, seed: int = 0, row_base: int = 0, u: np.ndar
     cnt = int(_L().or_sample(_p(p32), _p(u), n, row_base, m, seed, _p(idx), _p(w), cap))
     k = min(cnt, cap)
     return idx[:k].copy(), w[:k].copy(), cnt
+
+
+def sample_multinomial(p32: np.ndarray, m: int, seed: int = 0, row_base: int = 0):
+    """NEXT-4: m i.i.d. draws proportional to fp32 p from an exact fixed-point CDF (bit-exact integer
+    arithmetic; see oracle.c). Returns (idx[m], weight[m], T, F)."""
+    p32 = np.ascontiguousarray(p32, np.float32)
+    n = p32.shape[0]
+    idx = np.empty(max(m, 1), np.int64)
+    w = np.empty(max(m, 1), np.float64)
+    F = np.zeros(1, np.int32)
+    T = int(_L().or_sample_multinomial(_p(p32), n, m, seed, row_base, _p(idx), _p(w), _p(F)))
+    if T == 0:
+        raise ValueError("no positive probability")
+    return idx[:m].copy(), w[:m].copy(), T, int(F[0])

@@ -231,3 +231,49 @@ int64_t or_sample(const float* p, const double* u, int64_t n, int64_t row_base, 
   }
   return count;
 }
+
+/*
+ * NEXT-4: m i.i.d. draws with probability proportional to p_i from an exact fixed-point
+ * CDF (the multinomial reading of "sample m rows with probabilities p", P:L1258-1268 / P:L2178-2188):
+ *   F = 62 - ceil(log2 n) - e,  max_i p_i < 2^e (frexp)        -> sum_i W_i < 2^62
+ *   W_i = floor(p_i 2^F) (exact in fp64 -> uint64),  CDF_i = sum_{t <= i} W_t,  T = CDF_{n-1}
+ *   X_j = rng_u64(seed, 10, j) >> 11,  target_j = floor(X_j T / 2^53)   (128-bit product)
+ *   idx_j = row_base + min{i : CDF_i > target_j},  weight_j = (double)T / ((double)m (double)W_i)
+ * Returns T (0: no positive p) and writes F.  Integer arithmetic only: bit-exact.
+ */
+uint64_t or_sample_multinomial(const float* p, int64_t n, int64_t m, uint64_t seed, int64_t row_base, int64_t* idx,
+                               double* weight, int32_t* F_out) {
+  float mx = 0.f;
+  for (int64_t i = 0; i < n; ++i) if (p[i] > mx) mx = p[i];
+  if (!(mx > 0.f)) return 0;
+  int e = 0;
+  frexp((double)mx, &e);
+  int lg = 0;
+  while (((int64_t)1 << lg) < n) ++lg;
+  const int F = 62 - lg - e;
+  if (F_out) *F_out = F;
+  uint64_t* cdf = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)n);
+  uint64_t* W = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)n);
+  uint64_t acc = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double v = p[i] > 0.f ? floor(ldexp((double)p[i], F)) : 0.0;
+    W[i] = (uint64_t)v;
+    acc += W[i];
+    cdf[i] = acc;
+  }
+  const uint64_t T = acc;
+  for (int64_t j = 0; j < m && T > 0; ++j) {
+    const uint64_t X = or_rng_u64(seed, 10, (uint64_t)j) >> 11;
+    const uint64_t target = (uint64_t)(((unsigned __int128)X * (unsigned __int128)T) >> 53);
+    int64_t lo = 0, hi = n - 1;             /* first i with cdf[i] > target */
+    while (lo < hi) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (cdf[mid] > target) hi = mid; else lo = mid + 1;
+    }
+    idx[j] = row_base + lo;
+    weight[j] = (double)T / ((double)m * (double)W[lo]);
+  }
+  free(cdf);
+  free(W);
+  return T;
+}

@@ -16,6 +16,7 @@ from .api import (  # noqa: F401
     l1_rownorm_exact,
     l1_rownorm_probs,
     l1_sample,
+    l1_sample_multinomial,
     l1_sample_u,
     trim,
 )

@@ -204,6 +204,22 @@ def l1_probs_sample(lam, lambda_total, m: int, seed: int, row_base: int = 0, cap
     return p, idx, w, cnt
 
 
+def l1_sample_multinomial(p, m: int, seed: int, row_base: int = 0):
+    """NEXT-4: exactly m i.i.d. draws proportional to p (exact fixed-point CDF).
+    Returns (idx[m] int64, weight[m] fp64, total[1] uint64-as-int64) device tensors."""
+    L = _lib_()
+    _need(p, torch.float32, "p")
+    n = p.numel()
+    idx = torch.empty(m, dtype=torch.int64, device=p.device)
+    w = torch.empty(m, dtype=torch.float64, device=p.device)
+    tot = torch.zeros(1, dtype=torch.int64, device=p.device)
+    nb = L.l1_sample_multinomial_workspace_bytes(n)
+    ws = workspace(nb, "multinomial")
+    _lib.check(L.l1_sample_multinomial(_ptr(p), n, m, seed & 0xFFFFFFFFFFFFFFFF, row_base, _ptr(idx), _ptr(w),
+                                       _ptr(tot), _ptr(ws), ws.numel(), _stream()))
+    return idx, w, tot
+
+
 def trim(idx, w, cnt):
     """Host copies of the first min(count, capacity) samples."""
     c = int(cnt.item())

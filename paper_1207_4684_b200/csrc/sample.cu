@@ -325,3 +325,182 @@ extern "C" fct_status l1_probs_sample(const float* lambda, int64_t n, const doub
   FCT_LAUNCHED("probs_sample_kernel", st);
   return FCT_OK;
 }
+
+// ------------------------------------------------------------------------------------------------
+// NEXT-4: multinomial sampling -- m i.i.d. draws proportional to p from an exact
+// fixed-point CDF; integer arithmetic only, bit-exact with the oracle (oracle.c or_sample_multinomial):
+//   F = 62 - ceil(log2 n) - e (max p < 2^e),  W_i = floor(p_i 2^F),  CDF = inclusive scan of W (uint64),
+//   target_j = (X_j T) >> 53 with X_j = rng_u64(seed, 10, j) >> 11,  idx_j = first i with CDF_i > target_j,
+//   weight_j = (double)T / ((double)m (double)W_idx).
+namespace {
+
+__global__ void mn_max_kernel(const float* __restrict__ p, int64_t n, unsigned* __restrict__ mbits) {
+  unsigned m = 0u;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = p[i];
+    if (v > 0.f) m = max(m, __float_as_uint(v));   // positive floats order like their bit patterns
+  }
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(mbits, m);
+}
+__device__ __forceinline__ int mn_F(const unsigned* mbits, int lg) {
+  int e = 0;
+  frexp((double)__uint_as_float(*mbits), &e);
+  return 62 - lg - e;
+}
+__device__ __forceinline__ uint64_t mn_W(float v, int F) {
+  return v > 0.f ? (uint64_t)floor(ldexp((double)v, F)) : 0ull;
+}
+constexpr int kMnTile = 2048, kMnThreads = 256, kMnPer = kMnTile / kMnThreads;
+
+__global__ void __launch_bounds__(kMnThreads) mn_tile_sum_kernel(const float* __restrict__ p, int64_t n,
+                                                                  const unsigned* __restrict__ mbits, int lg,
+                                                                  uint64_t* __restrict__ tsum) {
+  if (*mbits == 0u) return;
+  const int F = mn_F(mbits, lg);
+  const int64_t base = (int64_t)blockIdx.x * kMnTile;
+  uint64_t s = 0;
+  for (int r = threadIdx.x; r < kMnTile; r += kMnThreads)
+    if (base + r < n) s += mn_W(p[base + r], F);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __shared__ uint64_t red[kMnThreads / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+    for (int w = 0; w < kMnThreads / 32; ++w) t += red[w];
+    tsum[blockIdx.x] = t;
+  }
+}
+// single CTA: exclusive scan of the tile sums in place, total -> *T (0 when no positive p)
+__global__ void __launch_bounds__(1024) mn_scan_kernel(uint64_t* __restrict__ tsum, int64_t ntiles,
+                                                        const unsigned* __restrict__ mbits, uint64_t* __restrict__ T) {
+  __shared__ uint64_t warp_tot[32];
+  __shared__ uint64_t carry;
+  if (*mbits == 0u) {
+    if (threadIdx.x == 0) *T = 0;
+    return;
+  }
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t b0 = 0; b0 < ntiles; b0 += blockDim.x) {
+    const int64_t i = b0 + threadIdx.x;
+    const uint64_t v = i < ntiles ? tsum[i] : 0;
+    uint64_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      uint64_t w = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_tot[lane] = w;
+    }
+    __syncthreads();
+    const uint64_t excl = carry + (warp > 0 ? warp_tot[warp - 1] : 0) + x - v;
+    if (i < ntiles) tsum[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *T = carry;
+}
+__global__ void __launch_bounds__(kMnThreads) mn_cdf_kernel(const float* __restrict__ p, int64_t n,
+                                                             const unsigned* __restrict__ mbits, int lg,
+                                                             const uint64_t* __restrict__ toff, uint64_t* __restrict__ cdf) {
+  if (*mbits == 0u) return;
+  const int F = mn_F(mbits, lg);
+  const int64_t base = (int64_t)blockIdx.x * kMnTile + (int64_t)threadIdx.x * kMnPer;
+  uint64_t w[kMnPer], s = 0;
+#pragma unroll
+  for (int r = 0; r < kMnPer; ++r) {
+    w[r] = base + r < n ? mn_W(p[base + r], F) : 0;
+    s += w[r];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t x = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __shared__ uint64_t wt[kMnThreads / 32];
+  if (lane == 31) wt[warp] = x;
+  __syncthreads();
+  uint64_t pre = toff[blockIdx.x];
+  for (int q = 0; q < warp; ++q) pre += wt[q];
+  uint64_t c = pre + x - s;
+#pragma unroll
+  for (int r = 0; r < kMnPer; ++r) {
+    c += w[r];
+    if (base + r < n) cdf[base + r] = c;
+  }
+}
+__global__ void mn_draw_kernel(const uint64_t* __restrict__ cdf, int64_t n, const uint64_t* __restrict__ Tp, int64_t m,
+                               uint64_t key, int64_t row_base, int64_t* __restrict__ idx, double* __restrict__ weight) {
+  const uint64_t T = *Tp;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+    if (T == 0) {
+      idx[j] = -1;
+      weight[j] = 0.0;
+      continue;
+    }
+    const uint64_t X = mix64(key + 0x9E3779B97F4A7C15ULL * (uint64_t)(j + 1)) >> 11;
+    const uint64_t hi = __umul64hi(X, T), lo = X * T;
+    const uint64_t target = (hi << 11) | (lo >> 53);
+    int64_t a = 0, b = n - 1;
+    while (a < b) {
+      const int64_t mid = a + (b - a) / 2;
+      if (cdf[mid] > target) b = mid; else a = mid + 1;
+    }
+    const uint64_t W = cdf[a] - (a > 0 ? cdf[a - 1] : 0ull);
+    idx[j] = row_base + a;
+    weight[j] = (double)T / ((double)m * (double)W);
+  }
+}
+
+}  // namespace
+
+extern "C" size_t l1_sample_multinomial_workspace_bytes(int64_t n) {
+  if (n < 1) return 0;
+  const size_t ntiles = (size_t)((n + kMnTile - 1) / kMnTile);
+  return fct::align256(sizeof(uint64_t) * (size_t)n) + fct::align256(sizeof(uint64_t) * ntiles) + fct::align256(8);
+}
+
+extern "C" fct_status l1_sample_multinomial(const float* p, int64_t n, int64_t m, uint64_t seed, int64_t row_base,
+                                            int64_t* idx, double* weight, uint64_t* total, void* workspace,
+                                            size_t workspace_bytes, void* stream) {
+  FCT_CHECK_ARG(p && idx && weight && total, FCT_ERR_ARG, "l1_sample_multinomial: NULL pointer");
+  FCT_CHECK_ARG(n >= 1 && row_base >= 0, FCT_ERR_SHAPE, "l1_sample_multinomial: n=%lld", (long long)n);
+  FCT_CHECK_ARG(m >= 1, FCT_ERR_ARG, "l1_sample_multinomial: m=%lld", (long long)m);
+  const size_t need = l1_sample_multinomial_workspace_bytes(n);
+  FCT_CHECK_ARG(workspace && workspace_bytes >= need, FCT_ERR_WORKSPACE,
+                "l1_sample_multinomial: workspace %zu < %zu bytes", workspace_bytes, need);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t ntiles = (n + kMnTile - 1) / kMnTile;
+  fct::Carver cv(workspace);
+  uint64_t* cdf = cv.take<uint64_t>((size_t)n);
+  uint64_t* tsum = cv.take<uint64_t>((size_t)ntiles);
+  unsigned* mbits = cv.take<unsigned>(2);
+  int lg = 0;
+  while ((1LL << lg) < n) ++lg;
+  FCT_CUDA_RET(cudaMemsetAsync(mbits, 0, sizeof(unsigned), st));
+  mn_max_kernel<<<fct::num_sms() * 4, 256, 0, st>>>(p, n, mbits);
+  FCT_LAUNCHED("mn_max_kernel", st);
+  mn_tile_sum_kernel<<<(unsigned)ntiles, kMnThreads, 0, st>>>(p, n, mbits, lg, tsum);
+  FCT_LAUNCHED("mn_tile_sum_kernel", st);
+  mn_scan_kernel<<<1, 1024, 0, st>>>(tsum, ntiles, mbits, total);
+  FCT_LAUNCHED("mn_scan_kernel", st);
+  mn_cdf_kernel<<<(unsigned)ntiles, kMnThreads, 0, st>>>(p, n, mbits, lg, tsum, cdf);
+  FCT_LAUNCHED("mn_cdf_kernel", st);
+  const uint64_t key = mix64(seed + 0x9E3779B97F4A7C15ULL * 11ULL);   // stream 10
+  mn_draw_kernel<<<(unsigned)std::min<int64_t>((m + 255) / 256, 4096), 256, 0, st>>>(cdf, n, total, m, key, row_base,
+                                                                                      idx, weight);
+  FCT_LAUNCHED("mn_draw_kernel", st);
+  return FCT_OK;
+}

@@ -28,7 +28,8 @@ def libpath():
 def test_header_declares_the_boundary():
     names = declared_functions()
     for must in ("fct_sketch", "l1_rownorm_probs", "l1_sample", "l1_rownorm", "l1_probs", "fct_condition",
-                 "fct_last_error", "fct_pipeline", "fct_pipeline_host", "l1_probs_sample"):
+                 "fct_last_error", "fct_pipeline", "fct_pipeline_host", "l1_probs_sample", "l1_rownorm_exact",
+                 "l1_sample_multinomial"):
         assert must in names
 
 

@@ -419,3 +419,26 @@ def test_rownorm_exact_identity_and_errors(fct):
             os.environ.pop("FCT_ROWNORM_SIMT", None)
         err = np.abs(lam.cpu().numpy().astype(np.float64) - lam_o)
         assert (err <= 2.0 ** -14 * bnd + 2.0 ** -17 * lam_o).all()
+
+
+# ---------------------------------------------------------------- NEXT-4: multinomial sampling (bit-exact)
+@pytest.mark.parametrize("n,m,row_base", [(1, 5, 0), (2047, 100, 0), (2049, 1000, 9), (300001, 4096, 123456),
+                                          (1 << 22, 65536, 1 << 30)])
+def test_sample_multinomial_bit_exact(fct, n, m, row_base):
+    rng = np.random.default_rng(n + m)
+    p = np.abs(rng.standard_cauchy(n)).astype(np.float32)
+    p[1::7] = 0.0
+    if n > 3:
+        p[2] = -1.0                     # negative / NaN entries count as zero probability on both sides
+        p[3] = np.nan
+    p[0] = max(p[0], 1e-3)
+    idx, w, tot = fct.l1_sample_multinomial(dev(p), m, seed=21, row_base=row_base)
+    oi, ow, oT, oF = oracle.sample_multinomial(p, m, seed=21, row_base=row_base)
+    assert int(tot.item()) == oT
+    np.testing.assert_array_equal(idx.cpu().numpy(), oi)
+    np.testing.assert_array_equal(w.cpu().numpy(), ow)
+
+
+def test_sample_multinomial_no_mass(fct):
+    idx, w, tot = fct.l1_sample_multinomial(dev(np.zeros(100, np.float32)), 7, seed=1)
+    assert int(tot.item()) == 0 and (idx.cpu().numpy() == -1).all() and (w.cpu().numpy() == 0).all()

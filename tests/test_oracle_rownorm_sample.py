@@ -213,3 +213,47 @@ def test_rownorm_exact_invariants_and_bound():
     for i in (0, 1, 100):
         want = math.fsum(abs(math.fsum(float(A[i, l]) * Rinv[l, j] for l in range(d))) for j in range(d))
         assert math.isclose(lam[i], want, rel_tol=1e-14)
+
+
+# ---------------------------------------------------------------- NEXT-4: multinomial m-draw sampling
+def test_multinomial_point_mass_and_zero_rows():
+    p = np.zeros(1000, np.float32)
+    p[417] = 0.25
+    idx, w, T, F = oracle.sample_multinomial(p, 64, seed=3)
+    assert (idx == 417).all() and np.all(w == 1.0 / 64)          # weight = 1 / (m * phat), phat = 1
+    rng = np.random.default_rng(5)
+    p = rng.random(5000).astype(np.float32)
+    p[::3] = 0.0
+    idx, w, T, F = oracle.sample_multinomial(p, 20000, seed=4, row_base=100)
+    assert (p[idx - 100] > 0).all()                                # zero rows never drawn
+    assert T < 2 ** 62 and T > 0
+
+
+def test_multinomial_uniform_closed_form():
+    """n a power of two, all p equal: every W_i is equal, so draw j is exactly floor(X_j n / 2^53) with
+    X_j the top 53 bits of the stream-10 generator (fctgen's independent copy of rng_u64)."""
+    n, m, seed = 1 << 12, 3000, 77
+    p = np.full(n, 1.0 / n, np.float32)
+    idx, w, T, F = oracle.sample_multinomial(p, m, seed=seed)
+    want = [(fctgen.rng_u64(seed, 10, j) >> 11) * n >> 53 for j in range(m)]
+    np.testing.assert_array_equal(idx, want)
+    np.testing.assert_allclose(w, n / m, rtol=1e-15)
+
+
+def test_multinomial_distribution_and_unbiased():
+    rng = np.random.default_rng(6)
+    n = 25
+    p = (rng.random(n) ** 3 + 0.01).astype(np.float32)      # every expected count >= 5 for the chi-square
+    idx, w, T, F = oracle.sample_multinomial(p, 200000, seed=9)
+    counts = np.bincount(idx, minlength=n)
+    expected = 200000 * p.astype(np.float64) / p.astype(np.float64).sum()
+    chi2 = ((counts - expected) ** 2 / expected).sum()
+    assert stats.chi2.sf(chi2, n - 1) > 1e-3
+    # Horvitz-Thompson: sum_j weight_j f(idx_j) is unbiased for sum_i f(i) (f = p-independent values)
+    f = rng.standard_normal(n) + 3.0
+    est = []
+    for s in range(300):
+        i2, w2, _, _ = oracle.sample_multinomial(p, 50, seed=1000 + s)
+        est.append(float((w2 * f[i2]).sum()))
+    est = np.array(est)
+    assert abs(est.mean() - f.sum()) < 3 * est.std(ddof=1) / math.sqrt(len(est)) + 1e-9
