@@ -200,6 +200,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-blocks", type=int, default=2560)
+    ap.add_argument("--estimator", default="median", choices=["median", "exact"],
+                    help="row norms: Cauchy median estimate (a8, default) or exact l1 norms of A R^-1 (NEXT-1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -232,7 +234,7 @@ def main():
     t_gen = time.perf_counter() - t_gen
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
     A, sg, cc, hh, pi2 = dev(inp.A), dev(inp.signs), dev(inp.cauchy), dev(inp.hash), dev(inp.pi2)
-    ops = cuda_ops()
+    ops = cuda_ops(args.estimator)
     names = ["start", "sketch", "allreduce_Y", "condition", "rownorm", "allreduce_sum", "sample"]
     K, W = args.steps, args.warmup
 
@@ -283,7 +285,7 @@ def main():
     t_rn = stage_ms["rownorm"]["mean"] * 1e-3
     kern = {"fct1_sketch": (sk_bytes, t_sk), "l1_rownorm": (rn_bytes, t_rn)}
     dom = max(kern, key=lambda k: kern[k][1])
-    traffic = load_traffic(cfg, n_loc, world)
+    traffic = load_traffic(cfg, n_loc, world) if args.estimator == "median" else {}
     rl = {}
     for kname, (byt, t) in kern.items():
         ach = byt / t / 1e9
@@ -339,7 +341,9 @@ def main():
                        "k": cfg.k, "m": cfg.m, "rows_per_gpu": sh.rows,
                        "l2": "inputs (A + aux = %.1f GB per GPU) >> 126 MB L2; no flush needed"
                              % ((sk_bytes) / 1e9),
-                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU"},
+                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+                       "row_norms": "Cauchy median estimate" if args.estimator == "median"
+                                    else "exact l1 norms of A R^-1 (NEXT-1)"},
             "hbm_gbs_sketch": sk["achieved"], "hbm_frac_sketch_of_8TBs": sk["frac_of_8TBs"],
             "roofline": roofline, "roofline_all": rl,
             "stages_ms": stage_ms, "gpu_launches": int(launches), "launches_per_step": launches / K,

@@ -49,14 +49,20 @@ class Ops:
     probs_sample: Callable | None = None   # fused: (lambda, total[1], m, seed, row_base) -> (p, idx, weight, count)
 
 
-def cuda_ops() -> Ops:
+def cuda_ops(estimator: str = "median") -> Ops:
+    """The CUDA compute steps.  estimator = "median" (the Cauchy median estimate of P:L2921-2938, a8) or
+    "exact" (NEXT-1: the exact l1 row norms of U = A R^-1 that the paper's Sec. 6.2 uses)."""
     from . import api
+    if estimator not in ("median", "exact"):
+        raise ValueError(f"estimator must be 'median' or 'exact', not {estimator!r}")
 
     def _cond(Y):
         R, Rinv, info = api.fct_condition(Y, check=False)
         return R, Rinv, info
 
     def _rown(A, Rinv, Pi2):
+        if estimator == "exact":
+            return api.l1_rownorm_exact(A, Rinv)
         return api.l1_rownorm(A, Rinv, Pi2)
 
     return Ops(sketch=lambda A, sg, c, h, s, r1: api.fct_sketch(A, sg, c, h, s, r1),
