@@ -165,6 +165,36 @@ fct_status l1_sample_multinomial(const float* p, int64_t n, int64_t m, uint64_t 
                                  int64_t* idx, double* weight, uint64_t* total, void* workspace,
                                  size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------------------------------------------------
+ * NEXT-2: the coreset l1 regression of FastCauchyRegression, steps 6-8
+ * (Thm P:L2955-2980: x_hat minimises ||D(Ax - b)||_1).  X = [A, -b]
+ * (P:L2915-2917): n x q fp32 row-major (ldx), the last column is -b.
+ *
+ * l1_coreset_gather: Z[j, :] = weight[j] * (double)X[idx[j] - row_base, :] for j < min(*count,
+ *   capacity) -- the rows of D X, so that sum_j |Z_j . [x; 1]| = ||D(Ax - b)||_1 over the sample.
+ *   idx/weight as written by l1_sample / l1_probs_sample / l1_sample_multinomial (device);
+ *   idx == NULL: rows 0..m-1; weight == NULL: 1; count == NULL: m = capacity (device int64 else).
+ *   Z: capacity x q fp64, row stride ldz >= q (device, caller-owned).  An index outside
+ *   [row_base, row_base + n) yields a NaN row (the solve then reports status 2).  Asynchronous.
+ * l1_lad_solve: x[0..q-2] = argmin_x sum_{j < m} |Z_j . [x; 1]| (m = *m, device int64, clamped to
+ *   capacity; m == NULL: capacity).  Primal-dual interior-point method (Mehrotra predictor-corrector)
+ *   on the LP  min 1'(u + v) s.t. Z[:, :q-1] x + u - v = -Z[:, q-1], u, v >= 0  and its dual
+ *   max b'y s.t. A'y = 0, |y| <= 1, in fp64; one cooperative kernel, nothing returns to the host.
+ *   Stops when f(x) - sum_j y_j rho_j(x) <= tol * max(f(x), 1e-5 f(0)) (f = the l1 objective at x,
+ *   rho = -Z.[x;1]) or
+ *   after max_iter iterations.  info (device, 8 doubles): [0] f(x), [1] sum y rho (dual value),
+ *   [2] relative gap, [3] iterations, [4] max |A'y|, [5] status (0 converged, 1 max_iter,
+ *   2 non-finite / breakdown), [6] m, [7] collapsed Cholesky pivots (rank-deficient coreset).
+ *   2 <= q <= 128.  workspace: l1_lad_workspace_bytes(capacity, q) device bytes.
+ */
+fct_status l1_coreset_gather(const float* X, int64_t n, int64_t q, int64_t ldx, const int64_t* idx,
+                             const double* weight, const int64_t* count, int64_t row_base,
+                             int64_t capacity, double* Z, int64_t ldz, void* stream);
+size_t l1_lad_workspace_bytes(int64_t capacity, int64_t q);
+fct_status l1_lad_solve(const double* Z, const int64_t* m, int64_t capacity, int64_t q, int64_t ldz,
+                        int32_t max_iter, double tol, double* x, double* info, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
 /* Fused a9 + a10 (what the pipeline runs): p[i] = (float)((double)lambda[i] / *lambda_total)
  * exactly as l1_probs, then the Bernoulli sampling of l1_sample on that p, in ONE pass over
  * lambda (single-pass decoupled look-back compaction).  Outputs (p, idx, weight, count) are

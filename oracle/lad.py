@@ -9,7 +9,8 @@ Written as the plain definition:
                 so that Z_j . [x; 1] = weight_j * (A_j x - b_j)
   lad           min_x sum_j |Z_j . [x; 1]| as the textbook LP
                     min 1'u + 1'v  s.t.  Z[:, :p] x + u - v = -Z[:, p],  u, v >= 0
-                solved by a library LP solver (scipy HiGHS dual simplex, a library primitive).
+                solved through its dual (p equality rows) by a library LP solver (scipy HiGHS dual
+                simplex, a library primitive); x from the dual's multipliers, strong duality checked.
   objective     sum_j |Z_j . [x; 1]| in fp64 (math.fsum, exactly rounded sum).
 Pinned in tests/test_oracle_lad.py by the weighted median (p = 1), brute-force vertex enumeration
 (an l1 optimum interpolates p rows), exact fits, equivariance and a subgradient optimality certificate.
@@ -37,8 +38,14 @@ def objective(Z: np.ndarray, x: np.ndarray) -> float:
 
 
 def lad(Z: np.ndarray):
-    """argmin_x sum_j |Z_j . [x; 1]| via the LP; returns (x, f) with f = objective(Z, x)."""
-    import scipy.sparse as sp
+    """argmin_x sum_j |Z_j . [x; 1]| via LP duality; returns (x, f) with f = objective(Z, x).
+
+    The l1 regression  min_x ||At x - bt||_1  (At = Z[:, :p], bt = -Z[:, p]) is the LP
+    min 1'u + 1'v s.t. At x + u - v = bt, u, v >= 0, whose dual is  max bt'y s.t. At'y = 0, -1 <= y <= 1.
+    The dual has p equality rows, so the library LP solver (HiGHS dual simplex) is fast on it; x is the
+    multiplier of At'y = 0: with V(c) = min {-bt'y : At'y = c, |y| <= 1} = -min_x (||At x - bt||_1 + c'x),
+    dV/dc = -x*, i.e. x = -(eqlin marginals).  Strong duality f(x) = bt'y* is checked on every call.
+    """
     from scipy.optimize import linprog
 
     Z = np.asarray(Z, dtype=np.float64)
@@ -47,16 +54,16 @@ def lad(Z: np.ndarray):
     if m == 0 or p == 0:
         x = np.zeros(p)
         return x, objective(Z, x) if m else 0.0
-    Aeq = sp.hstack([sp.csr_matrix(Z[:, :p]), sp.identity(m, format="csr"), -sp.identity(m, format="csr")],
-                    format="csr")
-    c = np.concatenate([np.zeros(p), np.ones(2 * m)])
-    bounds = [(None, None)] * p + [(0, None)] * (2 * m)
-    res = linprog(c, A_eq=Aeq, b_eq=-Z[:, p], bounds=bounds, method="highs-ds",
+    bt = -Z[:, p]
+    res = linprog(-bt, A_eq=Z[:, :p].T, b_eq=np.zeros(p), bounds=(-1, 1), method="highs-ds",
                   options={"primal_feasibility_tolerance": 1e-10, "dual_feasibility_tolerance": 1e-10})
     if res.status != 0:
         raise RuntimeError(f"oracle.lad: LP failed: {res.message}")
-    x = np.asarray(res.x[:p], dtype=np.float64)
-    return x, objective(Z, x)
+    x = -np.asarray(res.eqlin.marginals, dtype=np.float64)
+    f = objective(Z, x)
+    if not abs(f - (-res.fun)) <= 1e-9 * max(f, 1e-300) + 1e-12 * math.fsum(np.abs(bt).tolist()):
+        raise RuntimeError(f"oracle.lad: strong duality check failed: f(x) = {f!r}, dual = {-res.fun!r}")
+    return x, f
 
 
 def coreset_regression(X: np.ndarray, idx: np.ndarray, weight: np.ndarray, row_base: int = 0):

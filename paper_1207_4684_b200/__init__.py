@@ -10,6 +10,9 @@ from .api import (  # noqa: F401
     Pipeline,
     fct_condition,
     fct_sketch,
+    l1_coreset_gather,
+    l1_coreset_regression,
+    l1_lad_solve,
     l1_probs,
     l1_probs_sample,
     l1_rownorm,

@@ -220,6 +220,54 @@ def l1_sample_multinomial(p, m: int, seed: int, row_base: int = 0):
     return idx, w, tot
 
 
+def l1_coreset_gather(X, idx=None, weight=None, count=None, row_base: int = 0, capacity: int | None = None,
+                      Z=None):
+    """NEXT-2: Z = D X over the sampled rows (fp64), Z_j = weight_j * X[idx_j - row_base].
+    X: (n, q) fp32 CUDA, last column -b.  Returns Z (capacity, q) fp64."""
+    L = _lib_()
+    if X.dim() != 2 or X.dtype != torch.float32 or not X.is_cuda or X.stride(1) != 1:
+        raise ValueError("X must be a CUDA fp32 (n, q) tensor with unit column stride")
+    n, q = X.shape
+    if idx is not None:
+        _need(idx, torch.int64, "idx")
+    if weight is not None:
+        _need(weight, torch.float64, "weight")
+    if count is not None:
+        _need(count, torch.int64, "count")
+    if capacity is None:
+        capacity = idx.numel() if idx is not None else n
+    if Z is None:
+        Z = torch.empty((capacity, q), dtype=torch.float64, device=X.device)
+    _lib.check(L.l1_coreset_gather(_ptr(X), n, q, X.stride(0), _ptr(idx), _ptr(weight), _ptr(count), row_base,
+                                   capacity, _ptr(Z), Z.stride(0), _stream()))
+    return Z
+
+
+def l1_lad_solve(Z, m=None, max_iter: int = 100, tol: float = 1e-10):
+    """NEXT-2: x = argmin_x sum_{j<m} |Z_j . [x; 1]| (interior point, fp64, on the device).
+    Z: (capacity, q) fp64 CUDA; m: device int64 scalar tensor (rows used) or None (all rows).
+    Returns (x (q-1,) fp64, info (8,) fp64) device tensors (see include/fct.h)."""
+    L = _lib_()
+    _need(Z, torch.float64, "Z")
+    cap, q = Z.shape
+    if m is not None:
+        _need(m, torch.int64, "m")
+    x = torch.empty(q - 1, dtype=torch.float64, device=Z.device)
+    info = torch.empty(8, dtype=torch.float64, device=Z.device)
+    nb = L.l1_lad_workspace_bytes(cap, q)
+    ws = workspace(nb, "lad", Z.device)
+    _lib.check(L.l1_lad_solve(_ptr(Z), _ptr(m), cap, q, Z.stride(0), max_iter, tol, _ptr(x), _ptr(info), _ptr(ws),
+                              ws.numel(), _stream()))
+    return x, info
+
+
+def l1_coreset_regression(X, idx, weight, count, row_base: int = 0, max_iter: int = 100, tol: float = 1e-10):
+    """FastCauchyRegression steps 6-8 on one device: gather D X and solve min ||D(Ax - b)||_1.
+    Returns (x_hat, info)."""
+    Z = l1_coreset_gather(X, idx, weight, count, row_base)
+    return l1_lad_solve(Z, count, max_iter, tol)
+
+
 def trim(idx, w, cnt):
     """Host copies of the first min(count, capacity) samples."""
     c = int(cnt.item())
