@@ -29,7 +29,8 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int NT = 256;       // threads per CTA
-constexpr int RC = 32;        // rows per shared-memory chunk
+constexpr int RC = 64;        // rows per shared-memory chunk (NT / RC = 4 threads per row for the dot)
+static_assert(NT == 4 * RC, "phase A row dot uses 4 threads per row");
 constexpr int MAXQ = 128;     // q <= 128  ->  p <= 127
 constexpr int MT = 3;         // max 4x4 Gram tiles per thread (ceil(561 / 256))
 constexpr int NSC = 8;        // scalar partials per CTA
@@ -87,6 +88,61 @@ __device__ double block_min(double v, double* red_s) {
   return s;
 }
 
+// rows [c0, c0 + nr) of Z, columns [0, nc), into S (row stride SW), zero-padded to RC x P4; the loads of a
+// thread are issued together (8 in flight) before the shared stores
+__device__ __forceinline__ void load_chunk(double* __restrict__ S, const double* __restrict__ Z, int64_t ldz, int64_t c0,
+                                           int nr, int nc, int P4, int SW) {
+  const int total = RC * P4;
+  for (int e0 = threadIdx.x; e0 < total; e0 += 8 * NT) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * NT;
+      const int r = e / P4, j = e - r * P4;
+      v[u] = (e < total && r < nr && j < nc) ? Z[(c0 + r) * ldz + j] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * NT;
+      if (e < total) {
+        const int r = e / P4, j = e - r * P4;
+        S[r * SW + j] = v[u];
+      }
+    }
+  }
+}
+
+// a_i . xs for row i of Z with 4 threads per row (lanes 4r..4r+3), result in all four lanes
+__device__ __forceinline__ double row_dot4(const double* __restrict__ a, const double* __restrict__ xs, int p, bool ok) {
+  const int sub = threadIdx.x & 3;
+  double d = 0.0;
+  if (ok)
+    for (int j = sub; j < p; j += 4) d = fma(a[j], xs[j], d);
+  d += __shfl_xor_sync(0xffffffffu, d, 1);
+  d += __shfl_xor_sync(0xffffffffu, d, 2);
+  return d;
+}
+
+// reductions over the per-CTA partials: one load per thread, then a fixed-shape tree (deterministic)
+__device__ double parts_sum(const double* a, int n, double* red_s) {
+  double v = 0.0;
+  for (int c = threadIdx.x; c < n; c += NT) v += a[c];
+  return block_sum(v, red_s);
+}
+__device__ double parts_min(const double* a, int n, int stride, double* red_s) {
+  double v = 1e300;
+  for (int c = threadIdx.x; c < n; c += NT) v = fmin(v, a[(size_t)c * stride]);
+  return block_min(v, red_s);
+}
+// warp-cooperative sum of column e over n records of length PE (lanes take records c = lane, lane + 32, ...)
+__device__ __forceinline__ double warp_col_sum(const double* part, int n, int PE, int e) {
+  const int lane = threadIdx.x & 31;
+  double v = 0.0;
+  for (int c = lane; c < n; c += 32) v += part[(size_t)c * PE + e];
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __global__ void __launch_bounds__(NT, 1)
 lad_ipm_kernel(const double* __restrict__ Z, int64_t ldz, const int64_t* __restrict__ mptr, int64_t capacity, int q,
                int max_iter, double tol, Ws w, double* __restrict__ xout, double* __restrict__ info) {
@@ -94,13 +150,16 @@ lad_ipm_kernel(const double* __restrict__ Z, int64_t ldz, const int64_t* __restr
   const Geom g(q);
   const int p = g.p, tid = threadIdx.x, cta = blockIdx.x, ncta = gridDim.x;
   extern __shared__ __align__(16) double sm[];
-  // [chunk S: RC x SW] [theta_s RC] [y_s RC] [x_s MAXQ] [red_s 32] [G: p x (p+1) on CTA 0]
+  // [chunk S: RC x SW] [theta_s RC] [y_s RC] [x_s MAXQ] [red_s 32] [D0, RH, IV: MAXQ] [G: p x (p+1), CTA 0]
   double* S = sm;
   double* ths = S + (RC * g.SW > NT * 16 ? RC * g.SW : NT * 16);  // chunk | group-reduction staging
   double* yss = ths + RC;
   double* xs = yss + RC;
   double* red_s = xs + MAXQ;
-  double* G = red_s + 32;
+  double* D0 = red_s + 32;
+  double* RH = D0 + MAXQ;
+  double* IV = RH + MAXQ;  // 1 / L_kk
+  double* G = IV + MAXQ;
   const int GS = p + 1;  // row stride of G
 
   int64_t m = mptr ? *mptr : capacity;
@@ -126,8 +185,7 @@ lad_ipm_kernel(const double* __restrict__ Z, int64_t ldz, const int64_t* __restr
   if (cta == 0)
     for (int j = tid; j < p; j += NT) w.x[j] = 0.0;
   grid.sync();
-  double tot = 0.0;
-  for (int c = 0; c < ncta; ++c) tot += w.mus[c];
+  const double tot = parts_sum(w.mus, ncta, red_s);
   const double delta = m > 0 ? fmax(tot / (double)m, 1e-300) : 1.0;
   for (int64_t i = r0 + tid; i < r1; i += NT) {
     const double rh = -Z[i * ldz + p];
@@ -155,37 +213,36 @@ lad_ipm_kernel(const double* __restrict__ Z, int64_t ldz, const int64_t* __restr
     __syncthreads();
     for (int64_t c0 = r0; c0 < r1; c0 += RC) {
       const int nr = (int)min((int64_t)RC, r1 - c0);
-      for (int e = tid; e < RC * g.P4; e += NT) {
-        const int r = e / g.P4, j = e - r * g.P4;
-        S[r * g.SW + j] = (r < nr && j < q) ? Z[(c0 + r) * ldz + j] : 0.0;
-      }
+      load_chunk(S, Z, ldz, c0, nr, q, g.P4, g.SW);
       __syncthreads();
-      if (tid < RC) {
+      {
+        // rho_r = -(a_r . x + z_rp): 4 threads per row, lanes 4r..4r+3 take columns sub, sub + 4, ...
+        const int rr = tid >> 2, sub = tid & 3;
+        const double* a = S + rr * g.SW;
+        double d0 = 0.0;
+        for (int j = sub; j < p; j += 4) d0 = fma(a[j], xs[j], d0);
+        d0 += __shfl_xor_sync(0xffffffffu, d0, 1);
+        d0 += __shfl_xor_sync(0xffffffffu, d0, 2);
         double th = 0.0, yv = 0.0;
-        if (tid < nr) {
-          const int64_t i = c0 + tid;
-          const double* a = S + tid * g.SW;
-          double d0 = a[p], d1 = 0.0;
-          int j = 0;
-          for (; j + 1 < p; j += 2) {
-            d0 = fma(a[j], xs[j], d0);
-            d1 = fma(a[j + 1], xs[j + 1], d1);
-          }
-          if (j < p) d0 = fma(a[j], xs[j], d0);
-          const double rh = -(d0 + d1);
+        if (sub == 0 && rr < nr) {
+          const int64_t i = c0 + rr;
+          const double rh = -(d0 + a[p]);
           const double u = w.u[i], v = w.v[i], su = w.su[i], sv = w.sv[i];
           yv = w.y[i];
           th = 1.0 / (u / su + v / sv);
           w.th[i] = th;
           w.rho[i] = rh;
-          S[tid * g.SW + p] = rh;
           s_f += fabs(rh);
           s_yr += yv * rh;
           s_comp += u * su + v * sv;
           s_rp += fabs(rh - u + v);
         }
-        ths[tid] = th;
-        yss[tid] = yv;
+        __syncthreads();  // every lane of the row has read a[p] before it is replaced by rho
+        if (sub == 0) {
+          if (rr < nr) S[rr * g.SW + p] = -(d0 + a[p]);
+          ths[rr] = th;
+          yss[rr] = yv;
+        }
       }
       __syncthreads();
       for (int i = 0; i < ntile; ++i) {
@@ -237,22 +294,20 @@ lad_ipm_kernel(const double* __restrict__ Z, int64_t ldz, const int64_t* __restr
     }
     grid.sync();
     // ================= B: fixed-order reduction of the partial records
-    for (int e = cta * NT + tid; e < g.PE; e += ncta * NT) {
-      double s = 0.0;
-      for (int c = 0; c < ncta; ++c) s += w.part[(size_t)c * g.PE + e];
-      w.red[e] = s;
+    for (int e = cta * (NT / 32) + (tid >> 5); e < g.PE; e += ncta * (NT / 32)) {
+      const double s = warp_col_sum(w.part, ncta, g.PE, e);
+      if ((tid & 31) == 0) w.red[e] = s;
     }
     grid.sync();
     const double* scr = w.red + 16 * g.T + g.P4;
     f = scr[0];
     dual = scr[1];
     const double comp = scr[2];
-    gnorm = 0.0;
-    for (int j = 0; j < p; ++j) gnorm = fmax(gnorm, fabs(w.red[16 * g.T + j]));
     // relative gap, with an absolute floor at 1e-5 of the x = 0 objective (exact fits: f -> 0)
     const bool conv = m == 0 || f <= 1e-300 || (f - dual) <= tol * fmax(f, 1e-5 * f0);
     if (conv || it >= max_iter || !isfinite(f)) {
       status = conv ? 0 : (isfinite(f) ? 1 : 2);
+      for (int j = 0; j < p; ++j) gnorm = fmax(gnorm, fabs(w.red[16 * g.T + j]));
       break;
     }
     const double mu = comp / (2.0 * (double)m);
@@ -261,6 +316,7 @@ lad_ipm_kernel(const double* __restrict__ Z, int64_t ldz, const int64_t* __restr
       break;
     }
     // ================= C: CTA 0 factors G = At' Theta At and solves for the predictor direction
+    // (everything in shared memory: G/L, the original diagonal D0 and the right-hand side RH)
     if (cta == 0) {
       auto gram = [&](int j, int k) -> double {  // augmented Gram entry, j <= k
         const int J = j >> 2, K = k >> 2;
@@ -269,76 +325,78 @@ lad_ipm_kernel(const double* __restrict__ Z, int64_t ldz, const int64_t* __restr
       };
       for (int e = tid; e < p * p; e += NT) {
         const int j = e / p, k = e - j * p;
-        G[j * GS + k] = j <= k ? gram(j, k) : gram(k, j);
+        if (k <= j) G[j * GS + k] = gram(k, j);  // lower triangle
       }
-      for (int j = tid; j < p; j += NT) w.dxa[j] = gram(j, p) + w.red[16 * g.T + j];  // rhs: At'Theta rho + At'y
+      for (int j = tid; j < p; j += NT) {
+        D0[j] = gram(j, j);
+        RH[j] = gram(j, p) + w.red[16 * g.T + j];  // rhs: At'Theta rho + At'y
+      }
       __syncthreads();
       // Cholesky (lower, in place); a pivot that collapses relative to its original diagonal is replaced
-      // by 1e64 (that component of the step is dropped) -- the usual safeguard near the optimal face
+      // by 1e128 (that component of the step is dropped) -- the usual safeguard near the optimal face
+      const int wid = tid >> 5, lane = tid & 31;
       for (int k = 0; k < p; ++k) {
         if (tid == 0) {
           double piv = G[k * GS + k];
-          const double orig = gram(k, k);
-          if (!(piv > 1e-14 * orig) || !isfinite(piv)) {
+          if (!(piv > 1e-14 * D0[k]) || !isfinite(piv)) {
             piv = 1e128;
             ++nsing;
           }
-          G[k * GS + k] = sqrt(piv);
+          const double lkk = sqrt(piv);
+          G[k * GS + k] = lkk;
+          IV[k] = 1.0 / lkk;
         }
         __syncthreads();
-        const double lkk = G[k * GS + k];
-        for (int i = k + 1 + tid; i < p; i += NT) G[i * GS + k] /= lkk;
+        const double ilkk = IV[k];
+        for (int i = k + 1 + tid; i < p; i += NT) G[i * GS + k] *= ilkk;
         __syncthreads();
-        const int rem = p - k - 1;
-        for (int e = tid; e < rem * rem; e += NT) {
-          const int i = k + 1 + e / rem, j = k + 1 + e % rem;
-          if (j <= i) G[i * GS + j] -= G[i * GS + k] * G[j * GS + k];
+        for (int i = k + 1 + wid; i < p; i += NT / 32) {
+          const double lik = G[i * GS + k];
+          for (int j = k + 1 + lane; j <= i; j += 32) G[i * GS + j] -= lik * G[j * GS + k];
         }
         __syncthreads();
       }
     }
-    auto solve = [&](double* rhs) {  // CTA 0: rhs := (L L')^-1 rhs, in global memory, G holds L
-      for (int k = 0; k < p; ++k) {  // forward
-        if (tid == 0) rhs[k] /= G[k * GS + k];
-        __syncthreads();
-        const double wk = rhs[k];
-        for (int i = k + 1 + tid; i < p; i += NT) rhs[i] -= G[i * GS + k] * wk;
-        __syncthreads();
-      }
-      for (int k = p - 1; k >= 0; --k) {  // backward
-        if (tid == 0) rhs[k] /= G[k * GS + k];
-        __syncthreads();
-        const double wk = rhs[k];
-        for (int i = tid; i < k; i += NT) rhs[i] -= G[k * GS + i] * wk;
-        __syncthreads();
+    auto solve = [&](double* out) {  // CTA 0, warp 0: RH := (L L')^-1 RH, then out := RH
+      if (tid < 32) {
+        for (int k = 0; k < p; ++k) {  // forward
+          const double wk = RH[k] * IV[k];
+          __syncwarp();
+          if (tid == 0) RH[k] = wk;
+          for (int i = k + 1 + tid; i < p; i += 32) RH[i] -= G[i * GS + k] * wk;
+          __syncwarp();
+        }
+        for (int k = p - 1; k >= 0; --k) {  // backward
+          const double wk = RH[k] * IV[k];
+          __syncwarp();
+          if (tid == 0) RH[k] = wk;
+          for (int i = tid; i < k; i += 32) RH[i] -= G[k * GS + i] * wk;
+          __syncwarp();
+        }
+        for (int j = tid; j < p; j += 32) out[j] = RH[j];
+        __threadfence();
       }
     };
-    if (cta == 0) {
-      solve(w.dxa);
-      __threadfence();
-    }
+    if (cta == 0) solve(w.dxa);
     grid.sync();
     // ================= D: affine-scaling direction per row, step-length ratios
     for (int j = tid; j < MAXQ; j += NT) xs[j] = j < p ? w.dxa[j] : 0.0;
     __syncthreads();
     double ap = 1e300, ad = 1e300;
-    for (int64_t i = r0 + tid; i < r1; i += NT) {
-      const double* a = Z + i * ldz;
-      double d0 = 0.0, d1 = 0.0;
-      int j = 0;
-      for (; j + 1 < p; j += 2) {
-        d0 = fma(a[j], xs[j], d0);
-        d1 = fma(a[j + 1], xs[j + 1], d1);
+    for (int64_t b0 = r0; b0 < r1; b0 += NT / 4) {
+      const int64_t i = b0 + (tid >> 2);
+      const bool ok = i < r1;
+      const double ad_ = row_dot4(Z + (ok ? i : r0) * ldz, xs, p, ok);
+      if (ok && (tid & 3) == 0) {
+        const double u = w.u[i], v = w.v[i], su = w.su[i], sv = w.sv[i];
+        const double dy = w.th[i] * (w.rho[i] - ad_);
+        const double du = -u + u * dy / su, dv = -v - v * dy / sv;
+        w.dya[i] = dy;
+        ratio_min(u, du, ap);
+        ratio_min(v, dv, ap);
+        ratio_min(su, -dy, ad);
+        ratio_min(sv, dy, ad);
       }
-      if (j < p) d0 = fma(a[j], xs[j], d0);
-      const double u = w.u[i], v = w.v[i], su = w.su[i], sv = w.sv[i];
-      const double dy = w.th[i] * (w.rho[i] - (d0 + d1));
-      const double du = -u + u * dy / su, dv = -v - v * dy / sv;
-      w.dya[i] = dy;
-      ratio_min(u, du, ap);
-      ratio_min(v, dv, ap);
-      ratio_min(su, -dy, ad);
-      ratio_min(sv, dy, ad);
     }
     ap = block_min(ap, red_s);
     ad = block_min(ad, red_s);
@@ -348,12 +406,8 @@ lad_ipm_kernel(const double* __restrict__ Z, int64_t ldz, const int64_t* __restr
     }
     grid.sync();
     // ================= E: mu_aff
-    ap = 1e300;
-    ad = 1e300;
-    for (int c = 0; c < ncta; ++c) {
-      ap = fmin(ap, w.rat[2 * c]);
-      ad = fmin(ad, w.rat[2 * c + 1]);
-    }
+    ap = parts_min(w.rat, ncta, 2, red_s);
+    ad = parts_min(w.rat + 1, ncta, 2, red_s);
     const double apa = fmin(1.0, ap), ada = fmin(1.0, ad);
     double smu = 0.0;
     for (int64_t i = r0 + tid; i < r1; i += NT) {
@@ -365,19 +419,14 @@ lad_ipm_kernel(const double* __restrict__ Z, int64_t ldz, const int64_t* __restr
     if (tid == 0) w.mus[cta] = smu;
     grid.sync();
     // ================= F: corrector right-hand side At' Theta q_c
-    double mua = 0.0;
-    for (int c = 0; c < ncta; ++c) mua += w.mus[c];
-    mua /= 2.0 * (double)m;
+    const double mua = parts_sum(w.mus, ncta, red_s) / (2.0 * (double)m);
     double sig = mua / mu;
     sig = fmin(1.0, sig * sig * sig);
     const double tau = sig * mu;
     double hc = 0.0;
     for (int64_t c0 = r0; c0 < r1; c0 += RC) {
       const int nr = (int)min((int64_t)RC, r1 - c0);
-      for (int e = tid; e < RC * g.P4; e += NT) {
-        const int r = e / g.P4, j = e - r * g.P4;
-        S[r * g.SW + j] = (r < nr && j < p) ? Z[(c0 + r) * ldz + j] : 0.0;
-      }
+      load_chunk(S, Z, ldz, c0, nr, p, g.P4, g.SW);
       if (tid < RC) {
         double tq = 0.0;
         if (tid < nr) {
@@ -399,14 +448,12 @@ lad_ipm_kernel(const double* __restrict__ Z, int64_t ldz, const int64_t* __restr
     grid.sync();
     // ================= G: reduce, CTA 0 solves with the kept factor
     if (cta == 0) {
-      for (int j = tid; j < p; j += NT) {
-        double s = 0.0;
-        for (int c = 0; c < ncta; ++c) s += w.part[(size_t)c * g.PE + j];
-        w.dx[j] = s + w.red[16 * g.T + j];
+      for (int j = tid >> 5; j < p; j += NT / 32) {
+        const double s = warp_col_sum(w.part, ncta, g.PE, j);
+        if ((tid & 31) == 0) RH[j] = s + w.red[16 * g.T + j];
       }
       __syncthreads();
       solve(w.dx);
-      __threadfence();
     }
     grid.sync();
     // ================= H: combined direction per row, step-length ratios
@@ -414,28 +461,25 @@ lad_ipm_kernel(const double* __restrict__ Z, int64_t ldz, const int64_t* __restr
     __syncthreads();
     ap = 1e300;
     ad = 1e300;
-    for (int64_t i = r0 + tid; i < r1; i += NT) {
-      const double* a = Z + i * ldz;
-      double d0 = 0.0, d1 = 0.0;
-      int j = 0;
-      for (; j + 1 < p; j += 2) {
-        d0 = fma(a[j], xs[j], d0);
-        d1 = fma(a[j + 1], xs[j + 1], d1);
+    for (int64_t b0 = r0; b0 < r1; b0 += NT / 4) {
+      const int64_t i = b0 + (tid >> 2);
+      const bool ok = i < r1;
+      const double adx = row_dot4(Z + (ok ? i : r0) * ldz, xs, p, ok);
+      if (ok && (tid & 3) == 0) {
+        const double u = w.u[i], v = w.v[i], su = w.su[i], sv = w.sv[i], dya = w.dya[i];
+        const double dua = -u + u * dya / su, dva = -v - v * dya / sv;
+        const double gu = tau - u * su + dua * dya, gv = tau - v * sv - dva * dya;
+        const double qc = (w.rho[i] - u + v) - gu / su + gv / sv;
+        const double dy = w.th[i] * (qc - adx);
+        const double du = (gu + u * dy) / su, dv = (gv - v * dy) / sv;
+        w.du[i] = du;
+        w.dv[i] = dv;
+        w.dy[i] = dy;
+        ratio_min(u, du, ap);
+        ratio_min(v, dv, ap);
+        ratio_min(su, -dy, ad);
+        ratio_min(sv, dy, ad);
       }
-      if (j < p) d0 = fma(a[j], xs[j], d0);
-      const double u = w.u[i], v = w.v[i], su = w.su[i], sv = w.sv[i], dya = w.dya[i];
-      const double dua = -u + u * dya / su, dva = -v - v * dya / sv;
-      const double gu = tau - u * su + dua * dya, gv = tau - v * sv - dva * dya;
-      const double qc = (w.rho[i] - u + v) - gu / su + gv / sv;
-      const double dy = w.th[i] * (qc - (d0 + d1));
-      const double du = (gu + u * dy) / su, dv = (gv - v * dy) / sv;
-      w.du[i] = du;
-      w.dv[i] = dv;
-      w.dy[i] = dy;
-      ratio_min(u, du, ap);
-      ratio_min(v, dv, ap);
-      ratio_min(su, -dy, ad);
-      ratio_min(sv, dy, ad);
     }
     ap = block_min(ap, red_s);
     ad = block_min(ad, red_s);
@@ -445,12 +489,8 @@ lad_ipm_kernel(const double* __restrict__ Z, int64_t ldz, const int64_t* __restr
     }
     grid.sync();
     // ================= I: step
-    ap = 1e300;
-    ad = 1e300;
-    for (int c = 0; c < ncta; ++c) {
-      ap = fmin(ap, w.rat[2 * c]);
-      ad = fmin(ad, w.rat[2 * c + 1]);
-    }
+    ap = parts_min(w.rat, ncta, 2, red_s);
+    ad = parts_min(w.rat + 1, ncta, 2, red_s);
     const double alp = fmin(1.0, eta * ap), ald = fmin(1.0, eta * ad);
     for (int64_t i = r0 + tid; i < r1; i += NT) {
       w.u[i] += alp * w.du[i];
@@ -497,7 +537,7 @@ __global__ void coreset_gather_kernel(const float* __restrict__ X, int64_t n, in
 
 size_t lad_smem_bytes(int q) {
   const Geom g(q);
-  const size_t base = (size_t)RC * g.SW + 2 * RC + MAXQ + 32;
+  const size_t base = (size_t)RC * g.SW + 2 * RC + 4 * MAXQ + 32;
   const size_t stage = (size_t)NT * 16;  // group-reduction staging aliases the chunk region
   const size_t chunk = std::max((size_t)RC * g.SW, stage);
   return (chunk - (size_t)RC * g.SW + base + (size_t)g.p * (g.p + 1)) * sizeof(double);
