@@ -47,6 +47,8 @@ class Ops:
     probs: Callable       # (lambda, total[1]) -> p
     sample: Callable      # (p, m, seed, row_base) -> (idx, weight, count[1])
     probs_sample: Callable | None = None   # fused: (lambda, total[1], m, seed, row_base) -> (p, idx, weight, count)
+    coreset_gather: Callable | None = None  # NEXT-2: (X, idx, weight, k, row_base) -> Z (k, q) fp64 = rows of D X
+    lad_solve: Callable | None = None       # NEXT-2: (Z) -> (x, info)
 
 
 def cuda_ops(estimator: str = "median") -> Ops:
@@ -70,7 +72,10 @@ def cuda_ops(estimator: str = "median") -> Ops:
                probs=lambda lam, tot: api.l1_probs(lam, tot),
                sample=lambda p, m, seed, row_base: api.l1_sample(p, m, seed, row_base=row_base),
                probs_sample=lambda lam, tot, m, seed, row_base: api.l1_probs_sample(lam, tot, m, seed,
-                                                                                    row_base=row_base))
+                                                                                    row_base=row_base),
+               coreset_gather=lambda X, idx, w, k, row_base: api.l1_coreset_gather(X, idx[:k], w[:k], None,
+                                                                                   row_base=row_base, capacity=k),
+               lad_solve=lambda Z: api.l1_lad_solve(Z))
 
 
 @dataclass
@@ -135,3 +140,26 @@ def gather_samples(res: StepResult, group=None):
     out_i = [gi[r][:int(metas[r][0].item())] for r in range(world)]
     out_w = [gw[r][:int(metas[r][0].item())] for r in range(world)]
     return torch.cat(out_i), torch.cat(out_w), int(sum(int(m[1].item()) for m in metas))
+
+
+def coreset_regression(ops: Ops, shard: Shard, X, res: StepResult, group=None):
+    """NEXT-2 across ranks (FastCauchyRegression steps 6-8): every rank forms the rows of D X
+    for its own samples (X = [A, -b] is its row shard, row_base = shard.row0), ONE all-gather of the
+    k_r x q fp64 blocks assembles the coreset in rank order (= ascending global rows), and every rank solves
+    the identical small problem (no broadcast).  Returns (x_hat, info, Z)."""
+    k = min(int(res.count.item()), res.idx.numel())
+    Z = ops.coreset_gather(X, res.idx, res.weight, k, shard.row0)
+    if shard.world > 1:
+        world = dist.get_world_size(group)
+        meta = torch.tensor([k], dtype=torch.int64, device=Z.device)
+        metas = [torch.zeros_like(meta) for _ in range(world)]
+        dist.all_gather(metas, meta, group=group)
+        ks = [int(t.item()) for t in metas]
+        mx = max(1, max(ks))
+        pad = torch.zeros((mx, Z.shape[1]), dtype=Z.dtype, device=Z.device)
+        pad[:k] = Z
+        outs = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(outs, pad, group=group)
+        Z = torch.cat([o[:kr] for o, kr in zip(outs, ks)]).contiguous()
+    x, info = ops.lad_solve(Z)
+    return x, info, Z

@@ -15,7 +15,8 @@ import torch.multiprocessing as mp
 
 import fctgen
 import oracle
-from paper_1207_4684_b200.dist import Ops, run_step, gather_samples, shard_rows
+from oracle import lad as OL
+from paper_1207_4684_b200.dist import Ops, coreset_regression, run_step, gather_samples, shard_rows
 
 
 def test_shard_rows_cover_and_align():
@@ -51,7 +52,14 @@ def oracle_ops():
         idx, w, cnt = oracle.sample(p.numpy(), m, seed=seed, row_base=row_base)
         return torch.from_numpy(idx), torch.from_numpy(w), torch.tensor([cnt], dtype=torch.int64)
 
-    return Ops(sketch, condition, rownorm, probs, sample)
+    def coreset_gather(X, idx, w, k, row_base):
+        return torch.from_numpy(OL.coreset_rows(X.numpy(), idx[:k].numpy(), w[:k].numpy(), row_base))
+
+    def lad_solve(Z):
+        x, f = OL.lad(Z.numpy())
+        return torch.from_numpy(x), torch.tensor([f])
+
+    return Ops(sketch, condition, rownorm, probs, sample, coreset_gather=coreset_gather, lad_solve=lad_solve)
 
 
 def _free_port():
@@ -79,8 +87,10 @@ def _worker(rank, world, port, n, q):
         outs = [torch.zeros(L, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(outs, pad)
         lam = torch.cat([o[:x.numel()] for o, x in zip(outs, lam_all)])
+        xh, info, Z = coreset_regression(oracle_ops(), sh, t(inp.A), res)
         if rank == 0:
-            q.put((res.Y.numpy(), lam.numpy(), float(res.total.item()), gi.numpy(), gw.numpy(), gc))
+            q.put((res.Y.numpy(), lam.numpy(), float(res.total.item()), gi.numpy(), gw.numpy(), gc, Z.numpy(),
+                   xh.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -110,7 +120,7 @@ def test_dist_pipeline_equals_single_process(world):
         if p.is_alive():
             p.kill()
     assert got is not None and all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
-    Y, lam, tot, gi, gw, gc = got
+    Y, lam, tot, gi, gw, gc, Z, xh = got
     # single-process oracle pipeline on the full problem
     inp = fctgen.make_inputs(cfg, n=n)
     Y1, _ = oracle.sketch(inp.A, inp.signs, inp.cauchy, inp.hash, cfg.s, cfg.r1)
@@ -126,3 +136,8 @@ def test_dist_pipeline_equals_single_process(world):
     common = np.intersect1d(gi, i1)
     assert len(common) >= c1 - 2            # at most an ulp-level p difference may flip a decision
     assert (np.diff(gi) > 0).all()
+    # NEXT-2: the all-gathered coreset is exactly D X over the gathered samples, in ascending global rows,
+    # and its solution is the single-process one
+    np.testing.assert_array_equal(Z, OL.coreset_rows(inp.A, gi, gw))
+    x1, f1 = OL.lad(Z)
+    np.testing.assert_array_equal(xh, x1)
