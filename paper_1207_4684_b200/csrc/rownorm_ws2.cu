@@ -590,10 +590,11 @@ fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M3
 template <int KK, int DC>
 fct_status launch_k(const float* A, int64_t n, int d, int64_t lda, const float* M32, int KP32, const double* M64,
                     const float* colb, double* partial, int grid, float* lambda, cudaStream_t st) {
-  // variants (FCT_ROWNORM_VAR): 0 = 2 selection + 2 recompute groups, 1 = 3 groups that also (default)
-  // recompute, 2 = 2 groups that also recompute
+  // variants (FCT_ROWNORM_VAR): 0 = 2 selection + 2 recompute groups, 1 = 3 groups that also recompute,
+  // 2 = 2 groups that also recompute, 3 = 4 groups.  Default 1, and 3 at d = 32 (cfg 3 shape: 2.06 vs
+  // 2.18 ms measured; at d = 64 four groups cost the KEEP buffer and are 21 % slower)
   const char* ve = getenv("FCT_ROWNORM_VAR");
-  const int var = ve ? atoi(ve) : (getenv("FCT_ROWNORM_EG2") ? 2 : 1);
+  const int var = ve ? atoi(ve) : (getenv("FCT_ROWNORM_EG2") ? 2 : (d > 16 && d <= 32 ? 3 : 1));
 #define FCT_RN_LAUNCH(DD)                                                                                  \
   do {                                                                                                     \
     fct_status rc_ = FCT_ERR_UNSUPPORTED;                                                                  \
