@@ -148,7 +148,9 @@ struct AuxLayout {
   static constexpr int had_bytes = 8 * S;
 };
 
-template <int LA, int LB, int DT, int TL>
+// DIRECT (opt-in, FCT_SKETCH_DIRECT=1): the aux arrays are read from global memory (L2) instead of being
+// staged in shared memory, so more tile groups fit next to P (s = 2048, r1 = 8192: two groups instead of one)
+template <int LA, int LB, int DT, int TL, bool DIRECT>
 __global__ void __launch_bounds__(Geo<LA, LB, DT, TL>::THREADS, 1)
 sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, const int8_t* __restrict__ signs,
                  const float* __restrict__ cauchy, const int32_t* __restrict__ hash, int r1, int nslices,
@@ -160,8 +162,8 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
   // [TILES] tiles | [TILES] identity aux | [TILES] Hadamard aux | P[r1][DT]
   float* tiles = (float*)smraw;
   unsigned char* auxI0 = smraw + TILES * Gm::tile_bytes;
-  unsigned char* auxH0 = auxI0 + TILES * AL::id_bytes;
-  float* P = (float*)(auxH0 + TILES * AL::had_bytes);
+  unsigned char* auxH0 = auxI0 + (DIRECT ? 0 : TILES * AL::id_bytes);
+  float* P = (float*)(auxH0 + (DIRECT ? 0 : TILES * AL::had_bytes));
   __shared__ __align__(8) uint64_t bar_t[TILES], bar_i[TILES], bar_h[TILES];
 
   const int cs = blockIdx.x % nslices;
@@ -179,6 +181,7 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
   const int* sHi = (const int*)(auxI + AL::sign_bytes + 4 * S);
   const float* sCh = (const float*)auxH;
   const int* sHh = (const int*)(auxH + 4 * S);
+  (void)sSign; (void)sCi; (void)sHi; (void)sCh; (void)sHh;
 
   for (int e = threadIdx.x; e < r1 * DT; e += blockDim.x) P[e] = 0.f;
   if (threadIdx.x < TILES) {
@@ -202,6 +205,7 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
     return (int)(valid & ~15LL);
   };
   auto issue_id = [&](int64_t bb) {
+    if (DIRECT) return;
     const int sb = sign_bulk(bb);
     const int64_t t0 = 2 * bb * S;
     mbar_expect_tx(&bar_i[tg], (unsigned)(sb + 8 * S));
@@ -210,6 +214,7 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
     bulk_g2s(auxI + AL::sign_bytes + 4 * S, hash + t0 + S, 4u * S, &bar_i[tg]);
   };
   auto issue_had = [&](int64_t bb) {
+    if (DIRECT) return;
     const int64_t t0 = 2 * bb * S;
     mbar_expect_tx(&bar_h[tg], 8u * S);
     bulk_g2s(auxH, cauchy + t0, 4u * S, &bar_h[tg]);
@@ -229,9 +234,11 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
   for (; b < nblocks; b += bstep) {
     const int64_t bn = b + bstep;
     mbar_wait(&bar_t[tg], phase);
-    mbar_wait(&bar_i[tg], phase);
+    if (!DIRECT) mbar_wait(&bar_i[tg], phase);
     const int64_t rowb = b * S;
-    const int sb = sign_bulk(b);
+    const int sb = DIRECT ? 0 : sign_bulk(b);
+    const float* gC = cauchy + 2 * b * S;   // DIRECT: this block's aux in global memory
+    const int* gH = hash + 2 * b * S;
     // ---------------- phase A: rows g + (S/RA) k; identity half scattered from the staged aux
     {
       const int g = lt / DT;
@@ -250,8 +257,8 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
           if (r < sb) sg = sSign[r];
           else sg = rowb + r < n ? (int)__ldg(signs + rowb + r) : 0;
           x[k0 + q] *= (float)sg;
-          ad[q] = sHi[r] * DT + c;
-          vv[q] = (4.f * sCi[r]) * x[k0 + q];
+          ad[q] = (DIRECT ? __ldg(gH + S + r) : sHi[r]) * DT + c;
+          vv[q] = (4.f * (DIRECT ? __ldg(gC + S + r) : sCi[r])) * x[k0 + q];
         }
         smem_add_batch<BA>(P, ad, vv);
       }
@@ -274,7 +281,7 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     named_bar(1 + tg, NT);  // the tile buffer is free: prefetch the next block
     if (lt == 0 && bn < nblocks) issue_tile(bn);
-    mbar_wait(&bar_h[tg], phase);
+    if (!DIRECT) mbar_wait(&bar_h[tg], phase);
     phase ^= 1u;
 #pragma unroll
     for (int gi = 0; gi < NB; ++gi) {
@@ -284,8 +291,15 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
 #pragma unroll
       for (int k0 = 0; k0 < RB; k0 += 8) {
         const int r0 = RB * gp + k0;
-        const int4 h0 = *(const int4*)(sHh + r0), h1 = *(const int4*)(sHh + r0 + 4);
-        const float4 q0 = *(const float4*)(sCh + r0), q1 = *(const float4*)(sCh + r0 + 4);
+        int4 h0, h1;
+        float4 q0, q1;
+        if (DIRECT) {
+          h0 = __ldg((const int4*)(gH + r0)); h1 = __ldg((const int4*)(gH + r0 + 4));
+          q0 = __ldg((const float4*)(gC + r0)); q1 = __ldg((const float4*)(gC + r0 + 4));
+        } else {
+          h0 = *(const int4*)(sHh + r0); h1 = *(const int4*)(sHh + r0 + 4);
+          q0 = *(const float4*)(sCh + r0); q1 = *(const float4*)(sCh + r0 + 4);
+        }
         const int hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
         const float cw[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
         int ad[8];
@@ -322,7 +336,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-template <int LA, int LB, int DT, int TL>
+template <int LA, int LB, int DT, int TL, bool DIRECT>
 fct_status launch_v1(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs, const float* cauchy,
                      const int32_t* hash, int s, int r1, double* W, cudaStream_t st) {
   using Gm = Geo<LA, LB, DT, TL>;
@@ -339,9 +353,9 @@ fct_status launch_v1(const float* A, int64_t n, int64_t d, int64_t lda, const in
   FCT_CHECK_ARG(cr == CUDA_SUCCESS, FCT_ERR_CUDA, "fct_sketch: cuTensorMapEncodeTiled failed (%d)", (int)cr);
   const int nslices = (int)((d + DT - 1) / DT);
   const int64_t nblocks = (n + s - 1) / s;
-  const size_t smem = Gm::TILES * (Gm::tile_bytes + AuxLayout<Gm::S>::id_bytes + AuxLayout<Gm::S>::had_bytes) +
+  const size_t smem = Gm::TILES * (Gm::tile_bytes + (DIRECT ? 0 : AuxLayout<Gm::S>::id_bytes + AuxLayout<Gm::S>::had_bytes)) +
                       (size_t)r1 * DT * sizeof(float);
-  auto kern = sketch_v1_kernel<LA, LB, DT, TL>;
+  auto kern = sketch_v1_kernel<LA, LB, DT, TL, DIRECT>;
   FCT_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 1;
   FCT_CUDA_RET(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Gm::THREADS, smem));
@@ -360,10 +374,10 @@ fct_status launch_v1(const float* A, int64_t n, int64_t d, int64_t lda, const in
 
 constexpr size_t kV1Smem = 232448 - 256;   // max dynamic shared memory per block on sm_100, less static
 
-template <int LA, int LB, int DT, int TL>
+template <int LA, int LB, int DT, int TL, bool DIRECT>
 bool fits(int r1) {
   using Gm = Geo<LA, LB, DT, TL>;
-  return Gm::TILES * (Gm::tile_bytes + AuxLayout<Gm::S>::id_bytes + AuxLayout<Gm::S>::had_bytes) +
+  return Gm::TILES * (Gm::tile_bytes + (DIRECT ? 0 : AuxLayout<Gm::S>::id_bytes + AuxLayout<Gm::S>::had_bytes)) +
              (size_t)r1 * DT * sizeof(float) <= kV1Smem;
 }
 
@@ -375,14 +389,24 @@ fct_status fct_sketch_v1(const float* A, int64_t n, int64_t d, int64_t lda, cons
   if (((uintptr_t)A & 15) || ((uintptr_t)cauchy & 15) || ((uintptr_t)hash & 15) || ((uintptr_t)signs & 15) ||
       (lda % 4) || n >= (1LL << 31))
     return FCT_ERR_UNSUPPORTED;
-#define TRY(LA_, LB_, DT_, TL_)                                                              \
-  if (s == (1 << (LA_ + LB_)) && fits<LA_, LB_, DT_, TL_>(r1) && (DT_ <= 8 || d >= DT_))     \
-    return launch_v1<LA_, LB_, DT_, TL_>(A, n, d, lda, signs, cauchy, hash, s, r1, W, st);
-  // widest column slice that fits first (fewer aux re-reads, fewer bank conflicts), then narrower
+  const char* dv = getenv("FCT_SKETCH_DIRECT");   // 1: prefer the DIRECT-aux instances, 0: never use them
+  const int direct = dv ? atoi(dv) : -1;
+#define TRYD(LA_, LB_, DT_, TL_, DI_)                                                              \
+  if (s == (1 << (LA_ + LB_)) && fits<LA_, LB_, DT_, TL_, DI_>(r1) && (DT_ <= 8 || d >= DT_) &&   \
+      (DI_ ? direct != 0 : direct != 1))                                                            \
+    return launch_v1<LA_, LB_, DT_, TL_, DI_>(A, n, d, lda, signs, cauchy, hash, s, r1, W, st);
+#define TRY(LA_, LB_, DT_, TL_) TRYD(LA_, LB_, DT_, TL_, false)
+  if (direct == 1) {
+    TRYD(6, 5, 4, 2, true) TRYD(5, 5, 8, 3, true) TRYD(5, 5, 8, 2, true)
+  }
+  // widest column slice that fits first (fewer aux re-reads, fewer bank conflicts), then narrower.  DIRECT
+  // (opt-in) was measured without gain: cfg 5 shape 26.5 vs 26.0 ms (2 groups vs 1), cfg 4 15.7 vs 12.7 ms
+  // (3 groups vs 2) -- the kernel is bound by shared-memory wavefronts, not by latency
   TRY(6, 5, 16, 1) TRY(6, 5, 8, 2) TRY(6, 5, 4, 2) TRY(6, 5, 4, 1)        // s = 2048
   TRY(5, 5, 16, 1) TRY(5, 5, 8, 2) TRY(5, 5, 4, 4) TRY(5, 5, 4, 2)        // s = 1024
   TRY(4, 4, 16, 2) TRY(4, 4, 8, 4) TRY(4, 4, 4, 8)                        // s = 256
   TRY(3, 3, 8, 8) TRY(3, 3, 4, 8)                                         // s = 64
 #undef TRY
+#undef TRYD
   return FCT_ERR_UNSUPPORTED;
 }

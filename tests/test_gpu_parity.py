@@ -306,6 +306,17 @@ def test_sketch_v3_path_matches_too(fct, c, monkeypatch):
     assert_sketch_close(sketch_gpu(fct, inp), Yo, Mb)
 
 
+@pytest.mark.parametrize("c", [4, 5])
+@pytest.mark.parametrize("direct", ["0", "1"])
+def test_sketch_direct_aux_matches_too(fct, c, direct, monkeypatch):
+    """K1 with the aux read through L2 (DIRECT, opt-in) and with the staged default."""
+    monkeypatch.setenv("FCT_SKETCH_DIRECT", direct)
+    cfg = fctgen.CONFIGS[c]
+    inp = fctgen.make_inputs(cfg, n=9 * cfg.s + 5)
+    Yo, Mb = oracle.sketch(inp.A, inp.signs, inp.cauchy, inp.hash, cfg.s, cfg.r1)
+    assert_sketch_close(sketch_gpu(fct, inp), Yo, Mb)
+
+
 @pytest.mark.parametrize("c", [1, 2, 3, 4, 5])
 def test_sketch_generic_path_matches_too(fct, c, monkeypatch):
     """The generic (any s, d, lda) kernel stays parity-green: forced with FCT_SKETCH_GENERIC=1."""
