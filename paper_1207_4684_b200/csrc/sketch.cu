@@ -179,7 +179,9 @@ extern "C" fct_status fct_sketch(const float* A, int64_t n, int64_t d, int64_t l
   }
   fct_status rc = FCT_ERR_UNSUPPORTED;
   if (!getenv("FCT_SKETCH_GENERIC")) {
-    rc = fct_sketch_v3(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st);
+    rc = FCT_ERR_UNSUPPORTED;
+    if (getenv("FCT_SKETCH_V4")) rc = fct_sketch_v4(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st);
+    if (rc == FCT_ERR_UNSUPPORTED) rc = fct_sketch_v3(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st);
     if (rc == FCT_ERR_UNSUPPORTED) rc = fct_sketch_v1(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st);
   }
   if (rc == FCT_ERR_UNSUPPORTED) switch (dt) {

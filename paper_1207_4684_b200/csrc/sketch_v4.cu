@@ -1,0 +1,407 @@
+// sketch_v4.cu -- K1 v4: the v1 structure (sketch_v1.cu) with one thread per COLUMN PAIR: every value in
+// registers is a float2 (two adjacent columns of the slice), the FWHT butterflies are packed f32x2 adds, and
+// every scatter update is one 64-bit shared load + one 64-bit CAS for two columns, so a warp instruction
+// covers 8 bucket rows x 4 column pairs (v1: 4 rows x 8 columns, 32-bit) -- half the scatter instructions.
+// (Sec. 3.1; layout as in v1 below.)
+//
+// Per CTA: one column slice [c0, c0+DT) of the output, fp32 partial P[r1][DT] in shared memory for the
+// CTA's lifetime (flushed once into the fp64 workspace).  The CTA's threads form TILES independent
+// "tile groups" (NT threads each, own TMA buffer, own named barrier) that take row blocks round-robin.
+// Per block b (S = s rows) and tile group:
+//   TMA     tile[S][DT] <- A[bS : bS+S, c0 : c0+DT]            (zero fill past n / past d)
+//   phase A thread (c, g) holds rows g + (S/RA) k, k < RA (high row bits in registers):
+//           z = sign * a; identity half scatter P[h(2sb+s+r)][c] += 4 c_t z;
+//           LA butterfly stages; STS back with an XOR row swizzle
+//   phase B thread (c, g') holds rows RB g' + k, k < RB (low row bits): LDS; the buffer is now free
+//           -> the next block's TMA is issued; LB butterfly stages; Hadamard half scatter
+//           P[h(2sb+r)][c] += (4 c_t / sqrt(s)) (H_s z)_r
+// s = 2^(LA+LB).  Scatter-add into P uses shared-memory atomics (exclusive: any two threads may
+// hit the same bucket).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <math.h>
+#include "common.cuh"
+
+namespace {
+namespace v4 {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+
+// Batched shared-memory float2 add with ILP: 64-bit loads, then 64-bit CAS (ATOMS.CAS.64, compares both
+// columns), then a retry loop for the rare lanes whose word changed in between.  Exact: an update is applied
+// only by a successful CAS on the value it read.
+__device__ __forceinline__ unsigned long long f2u(float2 v) { return *(unsigned long long*)&v; }
+__device__ __forceinline__ float2 u2f(unsigned long long v) { return *(float2*)&v; }
+__device__ __forceinline__ float2 add2(float2 a, float2 b);
+template <int N>
+__device__ __forceinline__ void smem_add_batch2(float* __restrict__ P, const int (&addr)[N], const float2 (&val)[N]) {
+  unsigned long long old[N];
+#pragma unroll
+  for (int q = 0; q < N; ++q) old[q] = *(const unsigned long long*)&P[addr[q]];
+  unsigned pending = 0u;
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    const unsigned long long got =
+        atomicCAS((unsigned long long*)&P[addr[q]], old[q], f2u(add2(u2f(old[q]), val[q])));
+    if (got != old[q]) pending |= 1u << q;
+  }
+  while (pending) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      if ((pending >> q) & 1u) {
+        const unsigned long long o = *(volatile unsigned long long*)&P[addr[q]];
+        if (atomicCAS((unsigned long long*)&P[addr[q]], o, f2u(add2(u2f(o), val[q]))) == o) pending &= ~(1u << q);
+      }
+    }
+  }
+}
+
+template <int LA, int LB, int DT, int TILES_>
+struct Geo {
+  static constexpr int CP = DT / 2;             // column pairs per slice
+  static constexpr int S = 1 << (LA + LB);
+  static constexpr int RA = 1 << LA;            // float2 registers per thread in phase A
+  static constexpr int RB = 1 << LB;            // float2 registers per thread per group in phase B
+  static constexpr int NT = S * CP / RA;        // threads per tile group
+  static constexpr int NB = (S / RB) * CP / NT; // phase-B groups per thread
+  static constexpr int TILES = TILES_;
+  static constexpr int THREADS = NT * TILES;
+  static constexpr int G = CP >= 32 ? 1 : 32 / CP;  // rows per warp-instruction
+  static constexpr int BOXR = S < 256 ? S : 256;
+  static_assert(NT >= 32 && THREADS <= 1024 && TILES <= 15, "tile group size");
+  static_assert(NB >= 1 && RB >= G, "phase B layout");
+  static constexpr size_t tile_bytes = (size_t)S * DT * sizeof(float);
+};
+
+// physical row of logical row r in the exchange layout (conflict-free phase-B reads)
+template <int LB, int G>
+__device__ __forceinline__ int swz(int r) {
+  return G > 1 ? (r ^ ((r >> LB) & (G - 1))) : r;
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// packed fp32x2 add / sub (FADD2 on sm_100)
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long r, x = *(unsigned long long*)&a, y = *(unsigned long long*)&b;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+  return *(float2*)&r;
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  unsigned long long r, x = *(unsigned long long*)&a, y = *(unsigned long long*)&b;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+  return *(float2*)&r;
+}
+// in-register unnormalised Walsh-Hadamard transform of R float2 values (two columns at once, natural order)
+template <int R>
+__device__ __forceinline__ void fwht_regs2(float2 (&x)[R]) {
+#pragma unroll
+  for (int h = 1; h < R; h <<= 1)
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (!(k & h)) {
+        const float2 a = x[k], b = x[k + h];
+        x[k] = add2(a, b);
+        x[k + h] = sub2(a, b);
+      }
+}
+
+// aux bytes staged per block: identity half = signs[S] (padded to 16) + cauchy[S] + hash[S];
+// Hadamard half = cauchy[S] + hash[S]
+template <int S>
+struct AuxLayout {
+  static constexpr int sign_bytes = (S + 15) / 16 * 16;
+  static constexpr int id_bytes = sign_bytes + 8 * S;
+  static constexpr int had_bytes = 8 * S;
+};
+
+// DIRECT (opt-in, FCT_SKETCH_DIRECT=1): the aux arrays are read from global memory (L2) instead of being
+// staged in shared memory, so more tile groups fit next to P (s = 2048, r1 = 8192: two groups instead of one)
+template <int LA, int LB, int DT, int TL, bool DIRECT>
+__global__ void __launch_bounds__(Geo<LA, LB, DT, TL>::THREADS, 1)
+sketch_v4_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, const int8_t* __restrict__ signs,
+                 const float* __restrict__ cauchy, const int32_t* __restrict__ hash, int r1, int nslices,
+                 int64_t nblocks, float inv_sqrt_s, double* __restrict__ W) {
+  using Gm = Geo<LA, LB, DT, TL>;
+  using AL = AuxLayout<Gm::S>;
+  constexpr int S = Gm::S, RA = Gm::RA, RB = Gm::RB, NT = Gm::NT, NB = Gm::NB, TILES = Gm::TILES, G = Gm::G;
+  constexpr int CP = Gm::CP;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  // [TILES] tiles | [TILES] identity aux | [TILES] Hadamard aux | P[r1][DT]
+  float* tiles = (float*)smraw;
+  unsigned char* auxI0 = smraw + TILES * Gm::tile_bytes;
+  unsigned char* auxH0 = auxI0 + (DIRECT ? 0 : TILES * AL::id_bytes);
+  float* P = (float*)(auxH0 + (DIRECT ? 0 : TILES * AL::had_bytes));
+  __shared__ __align__(8) uint64_t bar_t[TILES], bar_i[TILES], bar_h[TILES];
+
+  const int cs = blockIdx.x % nslices;
+  const int grp = blockIdx.x / nslices;
+  const int ngrp = gridDim.x / nslices;
+  const int c0 = cs * DT;
+  const int tg = threadIdx.x / NT;        // tile group
+  const int lt = threadIdx.x - tg * NT;   // thread within the tile group
+  const int c = 2 * (lt % CP);            // first column of this thread's pair
+  float* tile = tiles + (size_t)tg * S * DT;
+  unsigned char* auxI = auxI0 + tg * AL::id_bytes;
+  unsigned char* auxH = auxH0 + tg * AL::had_bytes;
+  const int8_t* sSign = (const int8_t*)auxI;
+  const float* sCi = (const float*)(auxI + AL::sign_bytes);
+  const int* sHi = (const int*)(auxI + AL::sign_bytes + 4 * S);
+  const float* sCh = (const float*)auxH;
+  const int* sHh = (const int*)(auxH + 4 * S);
+  (void)sSign; (void)sCi; (void)sHi; (void)sCh; (void)sHh;
+
+  for (int e = threadIdx.x; e < r1 * DT; e += blockDim.x) P[e] = 0.f;
+  if (threadIdx.x < TILES) {
+    mbar_init(&bar_t[threadIdx.x], 1);
+    mbar_init(&bar_i[threadIdx.x], 1);
+    mbar_init(&bar_h[threadIdx.x], 1);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+
+  auto issue_tile = [&](int64_t bb) {
+    mbar_expect_tx(&bar_t[tg], (unsigned)Gm::tile_bytes);
+#pragma unroll
+    for (int q = 0; q < S / Gm::BOXR; ++q)
+      tma_load_2d(tile + (size_t)q * Gm::BOXR * DT, &tmap, c0, (int)(bb * S + q * Gm::BOXR), &bar_t[tg]);
+  };
+  // signs: bulk-copy the 16-byte-aligned prefix of the block's valid rows; the (rare) tail past it is
+  // read from global memory in phase A
+  auto sign_bulk = [&](int64_t bb) -> int {
+    const int64_t valid = n - bb * S < S ? n - bb * S : S;
+    return (int)(valid & ~15LL);
+  };
+  auto issue_id = [&](int64_t bb) {
+    if (DIRECT) return;
+    const int sb = sign_bulk(bb);
+    const int64_t t0 = 2 * bb * S;
+    mbar_expect_tx(&bar_i[tg], (unsigned)(sb + 8 * S));
+    if (sb > 0) bulk_g2s(auxI, signs + bb * S, (unsigned)sb, &bar_i[tg]);
+    bulk_g2s(auxI + AL::sign_bytes, cauchy + t0 + S, 4u * S, &bar_i[tg]);
+    bulk_g2s(auxI + AL::sign_bytes + 4 * S, hash + t0 + S, 4u * S, &bar_i[tg]);
+  };
+  auto issue_had = [&](int64_t bb) {
+    if (DIRECT) return;
+    const int64_t t0 = 2 * bb * S;
+    mbar_expect_tx(&bar_h[tg], 8u * S);
+    bulk_g2s(auxH, cauchy + t0, 4u * S, &bar_h[tg]);
+    bulk_g2s(auxH + 4 * S, hash + t0, 4u * S, &bar_h[tg]);
+  };
+
+  // blocks of this tile group: b = grp + ngrp * (tg + TILES * t)
+  const int64_t bstep = (int64_t)ngrp * TILES;
+  int64_t b = grp + (int64_t)ngrp * tg;
+  if (lt == 0 && b < nblocks) {
+    issue_tile(b);
+    issue_id(b);
+    issue_had(b);
+  }
+  unsigned phase = 0;
+  const float sc_h = 4.f * inv_sqrt_s;
+  for (; b < nblocks; b += bstep) {
+    const int64_t bn = b + bstep;
+    mbar_wait(&bar_t[tg], phase);
+    if (!DIRECT) mbar_wait(&bar_i[tg], phase);
+    const int64_t rowb = b * S;
+    const int sb = DIRECT ? 0 : sign_bulk(b);
+    const float* gC = cauchy + 2 * b * S;   // DIRECT: this block's aux in global memory
+    const int* gH = hash + 2 * b * S;
+    // ---------------- phase A: rows g + (S/RA) k; identity half scattered from the staged aux
+    {
+      const int g = lt / CP;
+      float2 x[RA];
+#pragma unroll
+      for (int k = 0; k < RA; ++k) x[k] = *(const float2*)&tile[(g + (S / RA) * k) * DT + c];
+      constexpr int BA = RA < 8 ? RA : 8;
+#pragma unroll
+      for (int k0 = 0; k0 < RA; k0 += BA) {
+        int ad[BA];
+        float2 vv[BA];
+#pragma unroll
+        for (int q = 0; q < BA; ++q) {
+          const int r = g + (S / RA) * (k0 + q);
+          int sg;
+          if (r < sb) sg = sSign[r];
+          else sg = rowb + r < n ? (int)__ldg(signs + rowb + r) : 0;
+          const float fs = (float)sg;
+          x[k0 + q] = make_float2(x[k0 + q].x * fs, x[k0 + q].y * fs);
+          ad[q] = (DIRECT ? __ldg(gH + S + r) : sHi[r]) * DT + c;
+          const float w = 4.f * (DIRECT ? __ldg(gC + S + r) : sCi[r]);
+          vv[q] = make_float2(w * x[k0 + q].x, w * x[k0 + q].y);
+        }
+        smem_add_batch2<BA>(P, ad, vv);
+      }
+      fwht_regs2<RA>(x);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      named_bar(1 + tg, NT);  // everyone has read the TMA tile and the identity aux
+      if (lt == 0 && bn < nblocks) issue_id(bn);
+#pragma unroll
+      for (int k = 0; k < RA; ++k) *(float2*)&tile[swz<LB, G>(g + (S / RA) * k) * DT + c] = x[k];
+    }
+    named_bar(1 + tg, NT);
+    // ---------------- phase B: rows RB g' + k
+    float2 y[NB][RB];
+#pragma unroll
+    for (int gi = 0; gi < NB; ++gi) {
+      const int gp = lt / CP + (NT / CP) * gi;
+#pragma unroll
+      for (int k = 0; k < RB; ++k) y[gi][k] = *(const float2*)&tile[swz<LB, G>(RB * gp + k) * DT + c];
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    named_bar(1 + tg, NT);  // the tile buffer is free: prefetch the next block
+    if (lt == 0 && bn < nblocks) issue_tile(bn);
+    if (!DIRECT) mbar_wait(&bar_h[tg], phase);
+    phase ^= 1u;
+#pragma unroll
+    for (int gi = 0; gi < NB; ++gi) {
+      const int gp = lt / CP + (NT / CP) * gi;
+      fwht_regs2<RB>(y[gi]);
+      static_assert(RB % 8 == 0, "phase B batches");
+#pragma unroll
+      for (int k0 = 0; k0 < RB; k0 += 8) {
+        const int r0 = RB * gp + k0;
+        int4 h0, h1;
+        float4 q0, q1;
+        if (DIRECT) {
+          h0 = __ldg((const int4*)(gH + r0)); h1 = __ldg((const int4*)(gH + r0 + 4));
+          q0 = __ldg((const float4*)(gC + r0)); q1 = __ldg((const float4*)(gC + r0 + 4));
+        } else {
+          h0 = *(const int4*)(sHh + r0); h1 = *(const int4*)(sHh + r0 + 4);
+          q0 = *(const float4*)(sCh + r0); q1 = *(const float4*)(sCh + r0 + 4);
+        }
+        const int hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        const float cw[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        int ad[8];
+        float2 vv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          ad[q] = hv[q] * DT + c;
+          const float w = sc_h * cw[q];
+          vv[q] = make_float2(w * y[gi][k0 + q].x, w * y[gi][k0 + q].y);
+        }
+        smem_add_batch2<8>(P, ad, vv);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    named_bar(1 + tg, NT);  // the Hadamard aux is free
+    if (lt == 0 && bn < nblocks) issue_had(bn);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < r1 * DT; e += blockDim.x) {
+    const int h = e / DT, cc = e - h * DT;
+    const float v = P[e];
+    if (c0 + cc < d && v != 0.f) atomicAdd(&W[(size_t)h * d + c0 + cc], (double)v);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+template <int LA, int LB, int DT, int TL, bool DIRECT>
+fct_status launch_v4(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs, const float* cauchy,
+                     const int32_t* hash, int s, int r1, double* W, cudaStream_t st) {
+  using Gm = Geo<LA, LB, DT, TL>;
+  auto enc = get_encode();
+  FCT_CHECK_ARG(enc, FCT_ERR_CUDA, "fct_sketch: cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)n};
+  cuuint64_t strides[1] = {(cuuint64_t)lda * sizeof(float)};
+  cuuint32_t box[2] = {(cuuint32_t)DT, (cuuint32_t)Gm::BOXR};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)A, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  FCT_CHECK_ARG(cr == CUDA_SUCCESS, FCT_ERR_CUDA, "fct_sketch: cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  const int nslices = (int)((d + DT - 1) / DT);
+  const int64_t nblocks = (n + s - 1) / s;
+  const size_t smem = Gm::TILES * (Gm::tile_bytes + (DIRECT ? 0 : AuxLayout<Gm::S>::id_bytes + AuxLayout<Gm::S>::had_bytes)) +
+                      (size_t)r1 * DT * sizeof(float);
+  auto kern = sketch_v4_kernel<LA, LB, DT, TL, DIRECT>;
+  FCT_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 1;
+  FCT_CUDA_RET(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Gm::THREADS, smem));
+  if (occ < 1) occ = 1;
+  // CTAs per slice: fill the SMs, and keep <= ~2048 expected terms per bucket per CTA partial
+  int64_t ngrp = ((int64_t)fct::num_sms() * occ) / nslices;
+  const int64_t min_grp = (2 * nblocks * (int64_t)s + 2048LL * r1 - 1) / (2048LL * r1);
+  ngrp = std::max<int64_t>(std::max<int64_t>(ngrp, 1), min_grp);
+  ngrp = std::min<int64_t>(ngrp, (nblocks + Gm::TILES - 1) / Gm::TILES);
+  if (ngrp < 1) ngrp = 1;
+  kern<<<(unsigned)(ngrp * nslices), Gm::THREADS, smem, st>>>(map, n, (int)d, signs, cauchy, hash, r1, nslices,
+                                                               nblocks, (float)(1.0 / sqrt((double)s)), W);
+  FCT_LAUNCHED("sketch_v4_kernel", st);
+  return FCT_OK;
+}
+
+constexpr size_t kV4Smem = 232448 - 256;   // max dynamic shared memory per block on sm_100, less static
+
+template <int LA, int LB, int DT, int TL, bool DIRECT>
+bool fits(int r1) {
+  using Gm = Geo<LA, LB, DT, TL>;
+  return Gm::TILES * (Gm::tile_bytes + (DIRECT ? 0 : AuxLayout<Gm::S>::id_bytes + AuxLayout<Gm::S>::had_bytes)) +
+             (size_t)r1 * DT * sizeof(float) <= kV4Smem;
+}
+
+
+}  // namespace v4
+}  // namespace
+
+// Returns FCT_ERR_UNSUPPORTED (without enqueueing) when no v4 instance covers (s, d, r1, alignment).
+fct_status fct_sketch_v4(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs, const float* cauchy,
+                         const int32_t* hash, int s, int r1, double* W, cudaStream_t st) {
+  using namespace v4;
+  if (((uintptr_t)A & 15) || ((uintptr_t)cauchy & 15) || ((uintptr_t)hash & 15) || ((uintptr_t)signs & 15) ||
+      (lda % 4) || n >= (1LL << 31))
+    return FCT_ERR_UNSUPPORTED;
+#define TRY(LA_, LB_, DT_, TL_)                                                                   \
+  if (s == (1 << (LA_ + LB_)) && fits<LA_, LB_, DT_, TL_, false>(r1) && (DT_ <= 8 || d >= DT_))   \
+    return launch_v4<LA_, LB_, DT_, TL_, false>(A, n, d, lda, signs, cauchy, hash, s, r1, W, st);
+  TRY(5, 5, 16, 1) TRY(5, 5, 8, 2) TRY(5, 5, 8, 1)        // s = 1024
+  TRY(4, 4, 16, 2) TRY(4, 4, 8, 4)                        // s = 256
+  TRY(3, 3, 8, 4)                                         // s = 64
+#undef TRY
+  return FCT_ERR_UNSUPPORTED;
+}
