@@ -94,6 +94,22 @@ def test_lad_exact_fit_and_empty(fct):
     assert info[5] == 0 and info[0] == 0.0 and info[6] == 0
 
 
+def test_lad_rank_deficient_and_wide_weights(fct):
+    """A duplicated column (rank-deficient coreset: collapsed Cholesky pivots, non-unique x) and Horvitz-Thompson
+    weights spanning 1 .. 1e6: the objective still reaches the LP optimum."""
+    rng = np.random.default_rng(11)
+    X = planted(3000, 6, 12).astype(np.float64)
+    Z = np.concatenate([X[:, :3], X[:, :1], X[:, 3:]], axis=1)       # column 0 repeated
+    Z *= np.exp(rng.uniform(0, np.log(1e6), (Z.shape[0], 1)))       # row weights 1 .. 1e6
+    Zd = dev(Z)
+    x, info = fct.l1_lad_solve(Zd, None, max_iter=200)
+    x, info = x.cpu().numpy(), info.cpu().numpy()
+    _, fo = OL.lad(Z)
+    fg = OL.objective(Z, x)
+    assert info[5] == 0 and info[7] >= 1       # converged, a pivot collapsed
+    assert fo * (1 - 1e-9) <= fg <= fo * (1 + F_TOL)
+
+
 def test_lad_count_prefix_and_clamp(fct):
     """m on the device selects a prefix of the capacity rows; m > capacity is clamped."""
     Z = planted(3000, 8, 9).astype(np.float64)
