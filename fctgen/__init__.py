@@ -179,3 +179,28 @@ def make_inputs(cfg: Config, n: int | None = None, row0: int = 0, s: int | None 
     h = hashes(seed, 2 * row0, 2 * n_pad, r1)
     pi2 = cauchy(seed, ST_PI2, 0, d * k).reshape(d, k)
     return Inputs(A, sg, c, h, pi2, s, r1, k, cfg.m, seed, row0)
+
+
+# ---------------------------------------------------------------- NEXT-3: FCT2 inputs (Sec. 3.2)
+ST_FCT2_SIGN, ST_FCT2_SEL, ST_FCT2_C = 10, 11, 12
+
+
+@dataclass
+class Fct2Inputs:
+    signs_t: np.ndarray   # int8[t], the Rademacher D_t of the SRHT G (same G in every block)
+    sel: np.ndarray       # int32[s], ascending distinct rows of H_t kept by R
+    C: np.ndarray         # float32[r1, nb * s], i.i.d. standard Cauchy
+    t: int
+    s: int
+    r1: int
+
+
+def fct2_inputs(seed: int, n: int, t: int, s: int, r1: int) -> Fct2Inputs:
+    """Seeded FCT2 randomness: D_t signs (top bit of the draw), R = the s smallest of t random keys (uniform
+    s-subset), C Cauchy on its own stream indexed row-major r * (nb s) + j."""
+    sg = np.where((rng_block(seed, ST_FCT2_SIGN, 0, t) >> np.uint64(63)) == 0, 1, -1).astype(np.int8)
+    keys = rng_block(seed, ST_FCT2_SEL, 0, t)
+    sel = np.sort(np.argsort(keys, kind="stable")[:s]).astype(np.int32)
+    nb = -(-n // t)
+    C = cauchy(seed, ST_FCT2_C, 0, r1 * nb * s).reshape(r1, nb * s)
+    return Fct2Inputs(sg, sel, C, t, s, r1)

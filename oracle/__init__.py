@@ -12,6 +12,7 @@ import this package.  It shares no code with paper_1207_4684_b200 (the CUDA path
   sample(...)     O4  Bernoulli l1 sampling   P:L1258-1268                        -> oracle.c
   sample_multinomial  NEXT-4  m i.i.d. draws from an exact fixed-point CDF          -> oracle.c
   lad.coreset_regression  NEXT-2  x_hat = argmin ||D(Ax - b)||_1 (LP)  -> lad.py
+  fct2.sketch     NEXT-3  Pi1 A = (8/r1) sqrt(pi t/2s) C H~ A, SRHT blocks (Sec. 3.2)  -> fct2.py
 Parity-unpinned items are listed in DESIGN.md ("Oracle pins").
 """
 from __future__ import annotations
