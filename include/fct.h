@@ -195,6 +195,22 @@ fct_status l1_lad_solve(const double* Z, const int64_t* m, int64_t capacity, int
                         int32_t max_iter, double tol, double* x, double* info, void* workspace,
                         size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------------------------------------------------
+ * NEXT-3: the FCT2 sketch (Sec. 3.2)
+ *   Y = Pi1 A,  Pi1 = (8 / r1) sqrt(pi t / (2 s)) * C * H~,  H~ = blockdiag(G, ..., G) over t-row blocks of A
+ *   (zero-padded to nb = ceil(n / t) blocks), G = sqrt(t / s) * R * (H_t / sqrt t) * D_t the SRHT the paper
+ *   uses as its FJLT, the SAME G in every block.
+ * signs_t: int8[t] (+-1) = D_t; sel: int32[s] distinct rows of H_t kept by R (in [0, t), not validated);
+ * C: r1 x (nb s) fp32 i.i.d. standard Cauchy, row-major with row stride ldc >= nb s (device, caller-owned).
+ * Y: r1 x d fp32 (overwritten).  t a power of two <= 32768, 1 <= s <= t, nb <= 65535.
+ * workspace: fct2_workspace_bytes(n, d, t, s, r1) device bytes (Z = H~ A in fp32 and an fp64 r1 x d
+ * accumulator).  Asynchronous on `stream`; argument errors are reported before anything is enqueued.
+ */
+size_t fct2_workspace_bytes(int64_t n, int64_t d, int32_t t, int32_t s, int32_t r1);
+fct_status fct2_sketch(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs_t,
+                       const int32_t* sel, const float* C, int64_t ldc, int32_t t, int32_t s, int32_t r1,
+                       float* Y, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Fused a9 + a10 (what the pipeline runs): p[i] = (float)((double)lambda[i] / *lambda_total)
  * exactly as l1_probs, then the Bernoulli sampling of l1_sample on that p, in ONE pass over
  * lambda (single-pass decoupled look-back compaction).  Outputs (p, idx, weight, count) are

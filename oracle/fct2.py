@@ -34,6 +34,19 @@ def hadamard(t: int) -> np.ndarray:
     return np.where(pc % 2 == 0, 1.0, -1.0)
 
 
+def hadamard_apply(X: np.ndarray) -> np.ndarray:
+    """H_t X (unnormalised, X: t x d).  t <= 1024: the explicit matrix; larger t: the Sylvester identity
+    H_{2^(a+b)} = H_{2^a} kron H_{2^b} (popcount(r & l) splits over the high and low index bits), i.e.
+    H_t X = H_{2^a} [X reshaped 2^a x 2^b x d] H_{2^b}^T, with both factors explicit."""
+    t = X.shape[0]
+    if t <= 1024:
+        return hadamard(t) @ X
+    a = (t.bit_length() - 1) // 2
+    ta, tb = 1 << a, t >> a
+    Y1 = (hadamard(ta) @ X.reshape(ta, -1)).reshape(ta, tb, -1)     # high index bits
+    return np.matmul(hadamard(tb), Y1).reshape(t, -1)                  # low index bits
+
+
 def scale(t: int, s: int, r1: int) -> float:
     """(8 / r1) sqrt(pi t / (2 s))."""
     return 8.0 / r1 * math.sqrt(math.pi * t / (2.0 * s))
@@ -44,14 +57,13 @@ def srht(A: np.ndarray, signs_t: np.ndarray, sel: np.ndarray, t: int, s: int) ->
     A = np.asarray(A, dtype=np.float64)
     n, d = A.shape
     nb = -(-n // t)
-    H = hadamard(t) / math.sqrt(t)
     D = np.asarray(signs_t, dtype=np.float64)
     Z = np.zeros((nb * s, d))
     for b in range(nb):
         Ab = np.zeros((t, d))
         rows = A[b * t:(b + 1) * t]
         Ab[:rows.shape[0]] = rows
-        Z[b * s:(b + 1) * s] = math.sqrt(t / s) * (H @ (D[:, None] * Ab))[np.asarray(sel)]
+        Z[b * s:(b + 1) * s] = math.sqrt(t / s) / math.sqrt(t) * hadamard_apply(D[:, None] * Ab)[np.asarray(sel)]
     return Z
 
 

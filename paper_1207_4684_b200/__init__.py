@@ -9,6 +9,7 @@ from .api import (  # noqa: F401
     HostPipeline,
     Pipeline,
     fct_condition,
+    fct2_sketch,
     fct_sketch,
     l1_coreset_gather,
     l1_coreset_regression,

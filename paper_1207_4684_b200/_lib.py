@@ -34,6 +34,8 @@ SIGNATURES = {
     "l1_coreset_gather": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "l1_lad_workspace_bytes": (_sz, [_i64, _i64]),
     "l1_lad_solve": (_int, [_vp, _vp, _i64, _i64, _i64, _i32, ctypes.c_double, _vp, _vp, _vp, _sz, _vp]),
+    "fct2_workspace_bytes": (_sz, [_i64, _i64, _i32, _i32, _i32]),
+    "fct2_sketch": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _sz, _vp]),
     "l1_probs_sample_workspace_bytes": (_sz, [_i64]),
     "l1_probs_sample": (_int, [_vp, _i64, _vp, _i64, _i64, _u64, _vp, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
     "fct_pipeline_workspace_bytes": (_sz, [_i64, _i64, _i32, _i32, _i32]),

@@ -268,6 +268,26 @@ def l1_coreset_regression(X, idx, weight, count, row_base: int = 0, max_iter: in
     return l1_lad_solve(Z, count, max_iter, tol)
 
 
+def fct2_sketch(A, signs_t, sel, C, t: int, s: int, r1: int, Y=None):
+    """NEXT-3: Y = (8/r1) sqrt(pi t/2s) C H~ A, the FCT2 sketch (Sec. 3.2) with SRHT blocks of t rows.
+    A: (n, d) fp32 CUDA (row stride lda); signs_t int8[t]; sel int32[s]; C: (r1, >= nb*s) fp32 CUDA."""
+    L = _lib_()
+    if A.dim() != 2 or A.dtype != torch.float32 or not A.is_cuda or A.stride(1) != 1:
+        raise ValueError("A must be a CUDA fp32 (n, d) tensor with unit column stride")
+    _need(signs_t, torch.int8, "signs_t")
+    _need(sel, torch.int32, "sel")
+    if C.dim() != 2 or C.dtype != torch.float32 or not C.is_cuda or C.stride(1) != 1:
+        raise ValueError("C must be a CUDA fp32 (r1, nb*s) tensor with unit column stride")
+    n, d = A.shape
+    if Y is None:
+        Y = torch.empty((r1, d), dtype=torch.float32, device=A.device)
+    nb = L.fct2_workspace_bytes(n, d, t, s, r1)
+    ws = workspace(nb, "fct2", A.device)
+    _lib.check(L.fct2_sketch(_ptr(A), n, d, A.stride(0), _ptr(signs_t), _ptr(sel), _ptr(C), C.stride(0), t, s, r1,
+                             _ptr(Y), _ptr(ws), ws.numel(), _stream()))
+    return Y
+
+
 def trim(idx, w, cnt):
     """Host copies of the first min(count, capacity) samples."""
     c = int(cnt.item())

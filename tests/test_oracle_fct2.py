@@ -27,6 +27,13 @@ def test_hadamard_is_sylvester(t):
     np.testing.assert_array_equal(F.hadamard(t), linalg.hadamard(t))
 
 
+@pytest.mark.parametrize("t", [2048, 4096])
+def test_kronecker_apply_matches_explicit(t):
+    """The large-t path (H_{2^a} kron H_{2^b}) equals the explicit Sylvester matrix (scipy)."""
+    X = np.random.default_rng(t).standard_normal((t, 3))
+    np.testing.assert_allclose(F.hadamard_apply(X), linalg.hadamard(t) @ X, rtol=1e-12, atol=1e-9)
+
+
 def test_s_equals_t_is_orthogonal():
     """R = identity (s = t): G = H_t/sqrt(t) D_t is orthogonal, so every column keeps its 2-norm per block."""
     rng = np.random.default_rng(0)
