@@ -13,6 +13,7 @@
 // This is the first correct version: the contraction is FP32-SIMT bound (r1 d nb s FMA).
 #include <math.h>
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace {
 
@@ -53,7 +54,8 @@ __device__ __forceinline__ void wht_pass(float* __restrict__ T, int t, int CS, i
 template <int LDT>   // DT = 2^LDT columns per CTA
 __global__ void __launch_bounds__(kSrhtThreads)
 srht_kernel(const float* __restrict__ A, int64_t n, int d, int64_t lda, const int8_t* __restrict__ signs_t,
-            const int32_t* __restrict__ sel, int t, int s, float inv_sqrt_s, float* __restrict__ Z, int ldz) {
+            const int32_t* __restrict__ sel, int t, int s, float inv_sqrt_s, float* __restrict__ Z, int ldz,
+            float* __restrict__ Zh, float* __restrict__ Zl, int64_t ldzt) {
   constexpr int DT = 1 << LDT;
   extern __shared__ float T[];   // [DT][CS], rows swizzled (phys); CS = t + 8 spreads the columns over the banks
   const int CS = t + 8;
@@ -93,6 +95,20 @@ srht_kernel(const float* __restrict__ A, int64_t n, int d, int64_t lda, const in
     }
     __syncthreads();
     lo += lb;
+  }
+  if (Zh) {
+    // transposed tf32 split for the tensor-core contraction: Zh[col][b s + i] = tf32(z), Zl = z - tf32(z)
+    for (int e = threadIdx.x; e < (s << LDT); e += blockDim.x) {
+      const int c = e / s, i = e - c * s;
+      const int col = c0 + c;
+      if (col < d) {
+        const float v = T[c * CS + phys(__ldg(sel + i))] * inv_sqrt_s;
+        const float hi = tcx::trunc_tf32(v);
+        Zh[(int64_t)col * ldzt + b * s + i] = hi;
+        Zl[(int64_t)col * ldzt + b * s + i] = v - hi;
+      }
+    }
+    return;
   }
   for (int e = threadIdx.x; e < (s << LDT); e += blockDim.x) {
     const int i = e >> LDT, c = e & (DT - 1);
@@ -180,12 +196,12 @@ int slice_width(int t) { return std::max(1, std::min(8, 32768 / t)); }   // <= 1
 
 template <int LDT>
 fct_status launch_srht(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs_t, const int32_t* sel,
-                       int t, int s, float* Z, int64_t nb, cudaStream_t st) {
+                       int t, int s, float* Z, float* Zh, float* Zl, int64_t ldzt, int64_t nb, cudaStream_t st) {
   constexpr int DT = 1 << LDT;
   const size_t smem = (size_t)DT * (t + 8) * sizeof(float);
   FCT_CUDA_RET(cudaFuncSetAttribute(srht_kernel<LDT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   srht_kernel<LDT><<<dim3((unsigned)((d + DT - 1) / DT), (unsigned)nb), kSrhtThreads, smem, st>>>(
-      A, n, (int)d, lda, signs_t, sel, t, s, (float)(1.0 / sqrt((double)s)), Z, (int)d);
+      A, n, (int)d, lda, signs_t, sel, t, s, (float)(1.0 / sqrt((double)s)), Z, (int)d, Zh, Zl, ldzt);
   FCT_LAUNCHED("fct2 srht_kernel", st);
   return FCT_OK;
 }
@@ -195,9 +211,10 @@ fct_status launch_srht(const float* A, int64_t n, int64_t d, int64_t lda, const 
 extern "C" size_t fct2_workspace_bytes(int64_t n, int64_t d, int32_t t, int32_t s, int32_t r1) {
   if (n < 1 || d < 1 || t < 1 || s < 1 || r1 < 1) return 0;
   const int64_t nb = (n + t - 1) / t;
+  const int64_t K = nb * s, ldzt = (K + 3) / 4 * 4;
   fct::Carver c(nullptr);
-  c.take<float>((size_t)(nb * s) * (size_t)d);   // Z
-  c.take<double>((size_t)r1 * (size_t)d);        // W
+  c.take<float>(std::max((size_t)K * (size_t)d, 2 * (size_t)d * (size_t)ldzt));   // Z, or Z^T hi | lo
+  c.take<double>((size_t)r1 * (size_t)d);                                       // W
   return c.off;
 }
 
@@ -217,27 +234,43 @@ extern "C" fct_status fct2_sketch(const float* A, int64_t n, int64_t d, int64_t 
                 workspace_bytes, need);
   cudaStream_t st = (cudaStream_t)stream;
   fct::Carver cv(workspace);
-  float* Z = cv.take<float>((size_t)K * (size_t)d);
+  const int64_t ldzt = (K + 3) / 4 * 4;
+  float* Z = cv.take<float>(std::max((size_t)K * (size_t)d, 2 * (size_t)d * (size_t)ldzt));
   double* W = cv.take<double>((size_t)r1 * (size_t)d);
-  // 1. Z = H~ A
-  fct_status rc = FCT_OK;
-  switch (slice_width(t)) {
-    case 8: rc = launch_srht<3>(A, n, d, lda, signs_t, sel, t, s, Z, nb, st); break;
-    case 4: rc = launch_srht<2>(A, n, d, lda, signs_t, sel, t, s, Z, nb, st); break;
-    case 2: rc = launch_srht<1>(A, n, d, lda, signs_t, sel, t, s, Z, nb, st); break;
-    default: rc = launch_srht<0>(A, n, d, lda, signs_t, sel, t, s, Z, nb, st); break;
-  }
-  if (rc != FCT_OK) return rc;
-  // 2. W = C Z (fp64 accumulation of fp32 partials), split-K to fill the GPU
   FCT_CUDA_RET(cudaMemsetAsync(W, 0, sizeof(double) * (size_t)r1 * d, st));
-  const int mt = (r1 + BM - 1) / BM, ntl = (int)((d + BN - 1) / BN);
-  int64_t splits = std::max<int64_t>(1, (int64_t)fct::num_sms() * 4 / (mt * ntl));
-  int64_t kchunk = (K + splits - 1) / splits;
-  kchunk = (kchunk + BK - 1) / BK * BK;
-  splits = (K + kchunk - 1) / kchunk;
-  FCT_CHECK_ARG(splits <= 65535, FCT_ERR_UNSUPPORTED, "fct2_sketch: too many K splits");
-  cz_kernel<<<dim3(mt, ntl, (unsigned)splits), 256, 0, st>>>(C, ldc, Z, (int)d, r1, (int)d, K, kchunk, W);
-  FCT_LAUNCHED("fct2 cz_kernel", st);
+  // tensor-core contraction unless its TMA constraints fail (or FCT2_SIMT=1)
+  const bool tc = !getenv("FCT2_SIMT") && ldc % 4 == 0 && ((uintptr_t)C & 15) == 0 && K < (1LL << 31);
+  auto srht = [&](float* Zr, float* Zh, float* Zl) -> fct_status {
+    switch (slice_width(t)) {
+      case 8: return launch_srht<3>(A, n, d, lda, signs_t, sel, t, s, Zr, Zh, Zl, ldzt, nb, st);
+      case 4: return launch_srht<2>(A, n, d, lda, signs_t, sel, t, s, Zr, Zh, Zl, ldzt, nb, st);
+      case 2: return launch_srht<1>(A, n, d, lda, signs_t, sel, t, s, Zr, Zh, Zl, ldzt, nb, st);
+      default: return launch_srht<0>(A, n, d, lda, signs_t, sel, t, s, Zr, Zh, Zl, ldzt, nb, st);
+    }
+  };
+  fct_status rc = FCT_ERR_UNSUPPORTED;
+  if (tc) {
+    float* Zh = Z;
+    float* Zl = Z + (size_t)d * ldzt;
+    // 1. Z^T = (H~ A)^T split into tf32 hi / lo;  2. W = C Z on tcgen05
+    rc = srht(nullptr, Zh, Zl);
+    if (rc != FCT_OK) return rc;
+    rc = fct2_cz_tc(C, ldc, Zh, Zl, ldzt, K, r1, (int)d, W, st);
+    if (rc != FCT_OK && rc != FCT_ERR_UNSUPPORTED) return rc;
+  }
+  if (rc == FCT_ERR_UNSUPPORTED) {
+    // 1. Z = H~ A;  2. W = C Z (SIMT, fp32 partials folded into fp64), split-K to fill the GPU
+    rc = srht(Z, nullptr, nullptr);
+    if (rc != FCT_OK) return rc;
+    const int mt = (r1 + BM - 1) / BM, ntl = (int)((d + BN - 1) / BN);
+    int64_t splits = std::max<int64_t>(1, (int64_t)fct::num_sms() * 4 / (mt * ntl));
+    int64_t kchunk = (K + splits - 1) / splits;
+    kchunk = (kchunk + BK - 1) / BK * BK;
+    splits = (K + kchunk - 1) / kchunk;
+    FCT_CHECK_ARG(splits <= 65535, FCT_ERR_UNSUPPORTED, "fct2_sketch: too many K splits");
+    cz_kernel<<<dim3(mt, ntl, (unsigned)splits), 256, 0, st>>>(C, ldc, Z, (int)d, r1, (int)d, K, kchunk, W);
+    FCT_LAUNCHED("fct2 cz_kernel", st);
+  }
   // 3. Y = kappa W
   const double kappa = 8.0 / r1 * sqrt(M_PI * (double)t / (2.0 * (double)s));
   const int64_t cnt = (int64_t)r1 * d;

@@ -38,8 +38,16 @@ def check(Yg, Yo, Mb, tol=1e-5):
     assert (err <= tol * Mb + 1e-30).all(), (err / np.maximum(Mb, 1e-300)).max()
 
 
+@pytest.fixture(params=["tc", "simt"])
+def path(request, monkeypatch):
+    """The tcgen05 3xTF32 contraction (default) and the SIMT one (FCT2_SIMT=1)."""
+    if request.param == "simt":
+        monkeypatch.setenv("FCT2_SIMT", "1")
+    return request.param
+
+
 @pytest.mark.parametrize("c", [1, 2, 3, 4, 5])
-def test_fct2_config_shapes(fct, c):
+def test_fct2_config_shapes(fct, c, path):
     """Each BASELINE config's matrix family and d with the paper's FCT2 parameters (s, t, r1) = params(d),
     3 blocks plus a ragged tail."""
     cfg = fctgen.CONFIGS[c]
@@ -53,7 +61,7 @@ def test_fct2_config_shapes(fct, c):
 
 @pytest.mark.parametrize("n,d,t,s,r1", [(1, 1, 1, 1, 1), (5, 3, 8, 8, 4), (100, 7, 64, 1, 9), (64, 2, 64, 64, 3),
                                         (1000, 65, 256, 17, 130), (2049, 9, 2048, 100, 70), (40000, 4, 32768, 50, 8)])
-def test_fct2_edges(fct, n, d, t, s, r1):
+def test_fct2_edges(fct, n, d, t, s, r1, path):
     """n < t (one partial block), t = 1, s = t (orthogonal G), s = 1, d > 64 (two output tiles), t = 32768."""
     rng = np.random.default_rng(n + d + t)
     A = rng.standard_normal((n, d)).astype(np.float32)
@@ -62,7 +70,7 @@ def test_fct2_edges(fct, n, d, t, s, r1):
     check(run(fct, A, inp), Yo, Mb)
 
 
-def test_fct2_strided_and_padded_C(fct):
+def test_fct2_strided_and_padded_C(fct, path):
     """lda > d and ldc > nb s (C with padding columns that must be ignored)."""
     rng = np.random.default_rng(3)
     n, d, t, s, r1 = 3000, 6, 512, 40, 33
