@@ -192,7 +192,7 @@ __global__ void finalize_kernel(const double* __restrict__ W, int64_t count, dou
     Y[i] = (float)(kappa * W[i]);
 }
 
-int slice_width(int t) { return std::max(1, std::min(8, 32768 / t)); }   // <= 128 KB tile (DT = 2 measured no faster at t = 8192)
+int slice_width(int t) { return std::max(1, std::min(8, 32768 / t)); }   // <= 128 KB tile (DT = 2 at t = 8192: 25.1 vs 20.8 ms)
 
 template <int LDT>
 fct_status launch_srht(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs_t, const int32_t* sel,
