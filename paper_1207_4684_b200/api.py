@@ -41,9 +41,10 @@ def _need(t: torch.Tensor, dtype, name: str, dev=True):
 
 
 def workspace(nbytes: int, tag: str = "default", device=None) -> torch.Tensor:
-    """A cached device byte buffer of at least nbytes (re-used across calls with the same tag)."""
+    """A cached device byte buffer of at least nbytes, re-used across calls with the same tag, device and
+    current stream (calls enqueued on different streams never share scratch memory)."""
     device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    key = (tag, device.index)
+    key = (tag, device.index, torch.cuda.current_stream(device).cuda_stream)
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
