@@ -332,50 +332,108 @@ lad_ipm_kernel(const double* __restrict__ Z, int64_t ldz, const int64_t* __restr
         RH[j] = gram(j, p) + w.red[16 * g.T + j];  // rhs: At'Theta rho + At'y
       }
       __syncthreads();
-      // Cholesky (lower, in place); a pivot that collapses relative to its original diagonal is replaced
-      // by 1e128 (that component of the step is dropped) -- the usual safeguard near the optimal face
+      // Cholesky (lower, in place), blocked by 8 columns: the diagonal block by warp 0 (warp-synchronous),
+      // the panel below it by one thread per row, the trailing update by warps over rows -- three CTA
+      // barriers per 8 columns.  A pivot that collapses relative to its original diagonal is replaced by
+      // 1e128 (that component of the step is dropped) -- the usual safeguard near the optimal face.
       const int wid = tid >> 5, lane = tid & 31;
-      for (int k = 0; k < p; ++k) {
-        if (tid == 0) {
-          double piv = G[k * GS + k];
-          if (!(piv > 1e-14 * D0[k]) || !isfinite(piv)) {
-            piv = 1e128;
-            ++nsing;
+      for (int k0 = 0; k0 < p; k0 += 8) {
+        const int kb = min(8, p - k0), ke = k0 + kb;
+        if (wid == 0) {
+          for (int k = k0; k < ke; ++k) {
+            if (lane == 0) {
+              double piv = G[k * GS + k];
+              if (!(piv > 1e-14 * D0[k]) || !isfinite(piv)) {
+                piv = 1e128;
+                ++nsing;
+              }
+              const double lkk = sqrt(piv);
+              G[k * GS + k] = lkk;
+              IV[k] = 1.0 / lkk;
+            }
+            __syncwarp();
+            if (lane < ke - k - 1) G[(k + 1 + lane) * GS + k] *= IV[k];
+            __syncwarp();
+            for (int e = lane; e < 64; e += 32) {   // rows i, cols j of the block, k < j <= i < ke
+              const int i = k + 1 + (e >> 3), j = k + 1 + (e & 7);
+              if (i < ke && j <= i) G[i * GS + j] -= G[i * GS + k] * G[j * GS + k];
+            }
+            __syncwarp();
           }
-          const double lkk = sqrt(piv);
-          G[k * GS + k] = lkk;
-          IV[k] = 1.0 / lkk;
         }
         __syncthreads();
-        const double ilkk = IV[k];
-        for (int i = k + 1 + tid; i < p; i += NT) G[i * GS + k] *= ilkk;
+        // panel: rows i >= ke solve X L_bb^T = G[i, k0:ke] (forward substitution over the block's columns)
+        for (int i = ke + tid; i < p; i += NT) {
+          double x[8];
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            if (kk < kb) {
+              double v = G[i * GS + k0 + kk];
+              for (int jj = 0; jj < kk; ++jj) v -= x[jj] * G[(k0 + kk) * GS + k0 + jj];
+              x[kk] = v * IV[k0 + kk];
+              G[i * GS + k0 + kk] = x[kk];
+            }
+          }
+        }
         __syncthreads();
-        for (int i = k + 1 + wid; i < p; i += NT / 32) {
-          const double lik = G[i * GS + k];
-          for (int j = k + 1 + lane; j <= i; j += 32) G[i * GS + j] -= lik * G[j * GS + k];
+        // trailing update G[i][j] -= sum_kk G[i][k0+kk] G[j][k0+kk], ke <= j <= i < p
+        for (int i = ke + wid; i < p; i += NT / 32) {
+          double li[8];
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) li[kk] = kk < kb ? G[i * GS + k0 + kk] : 0.0;
+          for (int j = ke + lane; j <= i; j += 32) {
+            double acc = G[i * GS + j];
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              if (kk < kb) acc -= li[kk] * G[j * GS + k0 + kk];
+            G[i * GS + j] = acc;
+          }
         }
         __syncthreads();
       }
     }
-    auto solve = [&](double* out) {  // CTA 0, warp 0: RH := (L L')^-1 RH, then out := RH
-      if (tid < 32) {
-        for (int k = 0; k < p; ++k) {  // forward
-          const double wk = RH[k] * IV[k];
-          __syncwarp();
-          if (tid == 0) RH[k] = wk;
-          for (int i = k + 1 + tid; i < p; i += 32) RH[i] -= G[i * GS + k] * wk;
-          __syncwarp();
+    auto solve = [&](double* out) {  // CTA 0: RH := (L L')^-1 RH (blocked by 8), then out := RH
+      const int wid = tid >> 5, lane = tid & 31;
+      for (int k0 = 0; k0 < p; k0 += 8) {  // forward: L w = RH
+        const int ke = min(p, k0 + 8);
+        if (wid == 0) {
+          for (int k = k0; k < ke; ++k) {
+            const double wk = RH[k] * IV[k];
+            __syncwarp();
+            if (lane == 0) RH[k] = wk;
+            if (lane < ke - k - 1) RH[k + 1 + lane] -= G[(k + 1 + lane) * GS + k] * wk;
+            __syncwarp();
+          }
         }
-        for (int k = p - 1; k >= 0; --k) {  // backward
-          const double wk = RH[k] * IV[k];
-          __syncwarp();
-          if (tid == 0) RH[k] = wk;
-          for (int i = tid; i < k; i += 32) RH[i] -= G[k * GS + i] * wk;
-          __syncwarp();
+        __syncthreads();
+        for (int i = ke + tid; i < p; i += NT) {
+          double v = RH[i];
+          for (int k = k0; k < ke; ++k) v -= G[i * GS + k] * RH[k];
+          RH[i] = v;
         }
-        for (int j = tid; j < p; j += 32) out[j] = RH[j];
-        __threadfence();
+        __syncthreads();
       }
+      for (int kb0 = (p - 1) / 8 * 8; kb0 >= 0; kb0 -= 8) {  // backward: L' x = w
+        const int ke = min(p, kb0 + 8);
+        if (wid == 0) {
+          for (int k = ke - 1; k >= kb0; --k) {
+            const double wk = RH[k] * IV[k];
+            __syncwarp();
+            if (lane == 0) RH[k] = wk;
+            if (lane < k - kb0) RH[kb0 + lane] -= G[k * GS + kb0 + lane] * wk;
+            __syncwarp();
+          }
+        }
+        __syncthreads();
+        for (int i = tid; i < kb0; i += NT) {
+          double v = RH[i];
+          for (int k = kb0; k < ke; ++k) v -= G[k * GS + i] * RH[k];
+          RH[i] = v;
+        }
+        __syncthreads();
+      }
+      for (int j = tid; j < p; j += NT) out[j] = RH[j];
+      __threadfence();
     };
     if (cta == 0) solve(w.dxa);
     grid.sync();
