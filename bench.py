@@ -50,6 +50,15 @@ def load_traffic(cfg, n_loc, world):
             return {}
         out = {k: v["dram_bytes_read"] + v["dram_bytes_write"] for k, v in m["kernels"].items()}
         out["_source"] = "profiles/r01_ncu_full_cfg4_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum)"
+        sk = m["kernels"].get("fct1_sketch", {})
+        if "smem_pipe_pct_of_peak" in sk:
+            # the sketch's measured limiter is the shared-memory data pipe, not DRAM (K1)
+            out["_limiter"] = {"fct1_sketch": {
+                "resource": "shared-memory data pipe (l1tex lsu wavefronts, 1 per cycle per SM)",
+                "pct_of_peak": sk["smem_pipe_pct_of_peak"],
+                "wavefronts_per_launch": sk["smem_wavefronts"],
+                "source": "profiles/r01_ncu_full_cfg4_traffic.json (l1tex__data_pipe_lsu_wavefronts_mem_shared.sum / "
+                          "(sm__cycles_elapsed.avg x 148))"}}
         return out
     except Exception:
         return {}
@@ -296,6 +305,8 @@ def main():
             rl[kname]["traffic_source"] = traffic["_source"]
     roofline = dict(rl[dom])
     roofline["kernel"] = dom
+    if traffic.get("_limiter", {}).get(dom):
+        roofline["limiter"] = traffic["_limiter"][dom]
     roofline["peak_source"] = peak_src
 
     # ---- e2e through the public API from pinned host buffers (N=1: HostPipeline / fct_pipeline_host)
