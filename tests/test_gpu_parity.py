@@ -203,6 +203,23 @@ def test_sample_bit_exact(fct, n, m, row_base):
     np.testing.assert_array_equal(gw.numpy(), ow)       # bitwise: 1/phat in IEEE fp64
 
 
+def test_device_uniforms_match_host_generator(fct):
+    """the device's u_i (rng_u64(seed, 9, row_base + i) >> 11) * 2^-53 equals fctgen's host copy
+    for 10^7 rows.  With m = 1: p_i = fp32(u_i) rounded down keeps no row iff every u_dev >= p_i, and p_i rounded
+    up keeps every row iff every u_dev < p_i -- together u_dev lies in u_host's fp32 interval on every row."""
+    n, seed, rb = 10_000_000, 77, 123457
+    u = fctgen.uniforms(seed, rb, n)
+    f = u.astype(np.float32)
+    lo = np.where(f.astype(np.float64) > u, np.nextafter(f, np.float32(0)), f)
+    hi = np.where(f.astype(np.float64) > u, f, np.nextafter(f, np.float32(2)))
+    assert (lo.astype(np.float64) <= u).all() and (hi.astype(np.float64) > u).all()
+    _, _, c_lo = fct.l1_sample(dev(lo), 1, seed, row_base=rb, capacity=16)
+    assert int(c_lo.item()) == 0
+    idx, w, c_hi = fct.l1_sample(dev(hi), 1, seed, row_base=rb, capacity=n)
+    assert int(c_hi.item()) == n
+    np.testing.assert_array_equal(idx.cpu().numpy(), rb + np.arange(n))
+
+
 def test_sample_explicit_uniforms_and_capacity(fct):
     n, m = 50000, 3000
     p = _probs(n, 5, heavy=False)
