@@ -333,6 +333,37 @@ def main():
                "path": "fct_pipeline_host (C ABI, pinned host buffers)"}
         del H, hA
 
+    # ---- e2e at N > 1 through the public multi-GPU API: every step copies the rank's shard from pinned host
+    # memory, runs dist.run_step (collectives included) and reads its samples back; max over ranks
+    if not args.no_e2e and world > 1:
+        pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+        hA, hs, hc, hh_, hp = pin(inp.A), pin(inp.signs), pin(inp.cauchy), pin(inp.hash), pin(inp.pi2)
+        ts, d2h = [], 0
+        for it in range(args.e2e_steps + 1):          # the first pass is a warm-up
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for dst, src in ((A, hA), (sg, hs), (cc, hc), (hh, hh_), (pi2, hp)):
+                dst.copy_(src, non_blocking=True)
+            r2 = step()
+            k = min(int(r2.count.item()), r2.idx.numel())   # D2H of the count (synchronises)
+            hi, hw = r2.idx[:k].cpu(), r2.weight[:k].cpu()
+            e1.record()
+            torch.cuda.synchronize()
+            if it > 0:
+                ts.append(e0.elapsed_time(e1))
+                d2h = 8 + k * 16
+        t_e = torch.tensor([sum(ts) / len(ts)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+        te = float(t_e.item())
+        h2d = hA.numel() * 4 + hs.numel() + hc.numel() * 4 + hh_.numel() * 4 + hp.numel() * 4
+        e2e = {"value": cfg.n / (te * 1e-3), "unit": "rows/s", "h2d_bytes_per_step": int(h2d) * world,
+               "d2h_bytes_per_step": int(d2h) * world, "ms_per_step": te, "steps": args.e2e_steps,
+               "path": "dist.run_step per rank from pinned host shards (H2D + step + D2H of the samples), "
+                       "max over ranks; bytes summed over ranks (rank 0's D2H x N)"}
+        del hA
+
     # ---- cpu baseline (rank 0, N=1 only): the oracle as it stands on a bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
