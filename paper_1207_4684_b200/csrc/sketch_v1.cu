@@ -256,7 +256,7 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
           int sg;
           if (r < sb) sg = sSign[r];
           else sg = rowb + r < n ? (int)__ldg(signs + rowb + r) : 0;
-          x[k0 + q] *= (float)sg;
+          x[k0 + q] = __int_as_float(__float_as_int(x[k0 + q]) ^ (sg & (int)0x80000000));   // sign flip, no I2F
           ad[q] = (DIRECT ? __ldg(gH + S + r) : sHi[r]) * DT + c;
           vv[q] = (4.f * (DIRECT ? __ldg(gC + S + r) : sCi[r])) * x[k0 + q];
         }
