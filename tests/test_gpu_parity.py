@@ -152,6 +152,20 @@ def test_rownorm_configs(fct, c):
     np.testing.assert_allclose(float(tot.item()), lam.sum(), rtol=1e-12)
 
 
+@pytest.mark.parametrize("c", [2, 4])
+def test_rownorm_gaussian_pi2(fct, c):
+    """NEXT-1's Gaussian-Pi2 estimator is the same kernel with Gaussian Pi2: parity at 1e-5."""
+    cfg = fctgen.CONFIGS[c]
+    inp = fctgen.make_inputs(cfg, n=2 * cfg.s)
+    Rinv = _rinv_for(inp)
+    Pi2 = fctgen.normals(cfg.seed, fctgen.ST_PI2, 0, cfg.d * cfg.k).reshape(cfg.d, cfg.k).astype(np.float32)
+    B = fctgen.matrix(cfg.kind, cfg.seed, max(cfg.n, 6000), cfg.d, 0, 6000 + 11)
+    lam_o, _ = oracle.rownorm(B, Rinv, Pi2)
+    lam, _ = fct.l1_rownorm(dev(B), dev(Rinv), dev(Pi2))
+    lam = lam.cpu().numpy().astype(np.float64)
+    assert (np.abs(lam - lam_o) <= LAM_TOL * lam_o + 1e-30).all()
+
+
 @pytest.mark.parametrize("k", [1, 2, 3, 7, 8, 16, 20, 27, 29, 32])
 def test_rownorm_all_k_and_identity(fct, k):
     rng = np.random.default_rng(k)

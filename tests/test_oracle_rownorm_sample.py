@@ -97,6 +97,25 @@ def test_median_of_half_cauchys_distribution(k):
         assert stats.ks_2samp(ratios, sim).pvalue > 1e-3
 
 
+@pytest.mark.parametrize("k", [9, 27])
+def test_median_of_half_normals_gaussian_pi2(k):
+    """NEXT-1's Gaussian-Pi2 estimator (OptimizedFastCauchyRegression): with Pi2 i.i.d. N(0,1),
+    lambda_i / ||U_(i)||_2 is the median of k i.i.d. half-normals (2-stability).  Odd k = 2h+1: exact CDF
+    I_{F(x)}(h+1, h+1) with F(x) = erf(x / sqrt 2); KS over 3000 draws of Pi2 for one row (Rinv = I)."""
+    d = 6
+    rng = np.random.default_rng(100 + k)
+    a = rng.standard_normal((1, d)).astype(np.float32)
+    l2 = float(np.linalg.norm(a.astype(np.float64)))
+    ratios = np.empty(3000)
+    for t in range(ratios.size):
+        Pi2 = rng.standard_normal((d, k)).astype(np.float32)
+        lam, _ = oracle.rownorm(a, np.eye(d), Pi2)
+        ratios[t] = lam[0] / l2
+    h = k // 2
+    cdf = lambda x: special.betainc(h + 1, h + 1, special.erf(x / math.sqrt(2)))
+    assert stats.kstest(ratios, cdf).pvalue > 1e-3
+
+
 # ---------------------------------------------------------------- O4: Bernoulli l1 sampling (P:L1258-1268)
 def test_sample_extremes_and_weights():
     n = 1000
