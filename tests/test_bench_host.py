@@ -1,0 +1,55 @@
+"""Host-side pieces of bench.py (no GPU): the roofline inputs it reads from profiles/, the metric name and the
+workload description, and the reference arm's JSON contract on a tiny sample."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+import fctgen
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+
+
+def test_metric_is_baselines():
+    with open(os.path.join(ROOT, "BASELINE.json")) as f:
+        assert json.load(f)["metric"] == bench.METRIC
+
+
+def test_traffic_and_limiter_only_for_the_captured_workload():
+    cfg = fctgen.CONFIGS[4]
+    t = bench.load_traffic(cfg, cfg.n, 1)
+    assert t["fct1_sketch"] > 0 and t["l1_rownorm"] > 0 and "dram__bytes_read.sum" in t["_source"]
+    lim = t["_limiter"]["fct1_sketch"]
+    assert 0 < lim["pct_of_peak"] <= 100 and lim["wavefronts_per_launch"] > 0
+    # another shard size or world size is not the captured launch: no traffic claimed
+    assert bench.load_traffic(cfg, cfg.n // 2, 2) == {}
+    assert bench.load_traffic(fctgen.CONFIGS[3], fctgen.CONFIGS[3].n, 1) == {}
+
+
+def test_peaks_have_a_source():
+    peak, src = bench.load_peaks()
+    assert peak > 1000 and isinstance(src, str) and src
+
+
+def test_workload_description_names_the_config():
+    cfg = fctgen.CONFIGS[4]
+    w = bench.workload_desc(cfg, cfg.n)
+    assert "cfg4" in w and str(cfg.n) in w and f"r1={cfg.r1}" in w
+
+
+def test_reference_arm_json_line():
+    """--impl reference (the oracle on the host cores) prints one JSON line with the contract's keys."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "1",
+                          "--steps", "1", "--warmup", "1", "--cpu-blocks", "2"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "config",
+              "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0 and line["warmup"] >= 3
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "oracle"
