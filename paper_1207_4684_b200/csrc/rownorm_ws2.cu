@@ -536,8 +536,10 @@ fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M3
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   FCT_CHECK_ARG(cr == CUDA_SUCCESS, FCT_ERR_CUDA, "l1_rownorm: cuTensorMapEncodeTiled failed (%d)", (int)cr);
   const int nch = (d + 31) / 32, KP = nch * 32;
-  // A_hi from TMEM when it fits next to EG + 1 accumulators (else from shared memory, SS form)
-  const bool at = 4 * KP + 64 * (EG + 1) <= 512 && !getenv("FCT_ROWNORM_ASS");
+  // A_hi from shared memory (SS form, default): the TMEM it would take holds 6 instead of 4 accumulators at
+  // d = 64, measured 1.0 % faster at cfg 4 (7.50 vs 7.57 ms) and 0.6 % at cfg 3.  FCT_ROWNORM_ATS=1 feeds A_hi
+  // from TMEM (TS form) when it fits next to EG + 1 accumulators.
+  const bool at = 4 * KP + 64 * (EG + 1) <= 512 && getenv("FCT_ROWNORM_ATS");
   const int ND = std::min(8, (512 - 2 * (at ? 2 * KP : KP)) / 64);
   int NA = 0;
   for (int na = 8; na >= 2; --na)

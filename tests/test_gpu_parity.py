@@ -382,7 +382,8 @@ def test_rownorm_simt_path_matches_too(fct, c, monkeypatch):
     assert (np.abs(lam - lam_o) <= LAM_TOL * lam_o).all()
 
 
-@pytest.mark.parametrize("env", ["FCT_ROWNORM_WS1", "FCT_ROWNORM_EG2", "FCT_ROWNORM_NOKEEP", "FCT_ROWNORM_VAR=0", None])
+@pytest.mark.parametrize("env", ["FCT_ROWNORM_WS1", "FCT_ROWNORM_EG2", "FCT_ROWNORM_NOKEEP", "FCT_ROWNORM_VAR=0",
+                                 "FCT_ROWNORM_ATS", None])
 @pytest.mark.parametrize("c", [2, 4, 5])
 def test_rownorm_tc_variants(fct, c, env, monkeypatch):
     """Each tcgen05 row-norm variant (ws2 with 3 or 2 epilogue groups, the older ws) is parity-green,
