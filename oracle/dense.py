@@ -46,3 +46,13 @@ def dense_sketch(A: np.ndarray, signs, cauchy, hash_rows, s: int, r1: int) -> np
     B, C, Ht, D = materialise(n, signs, cauchy, hash_rows, s, r1)
     A_pad = np.vstack([A, np.zeros((D.shape[0] - n, A.shape[1]))])
     return 4.0 * (B @ (C @ (Ht @ (D @ A_pad))))
+
+
+def dense_magnitude_bound(A: np.ndarray, signs, cauchy, hash_rows, s: int, r1: int) -> np.ndarray:
+    """north_star's entrywise tolerance yardstick 4 |B| |C| |H~| |D| |A_pad|, every factor materialised and
+    replaced by its entrywise absolute value before the products (the same matrices as dense_sketch)."""
+    A = np.asarray(A, np.float64)
+    n = A.shape[0]
+    B, C, Ht, D = materialise(n, signs, cauchy, hash_rows, s, r1)
+    A_pad = np.vstack([A, np.zeros((D.shape[0] - n, A.shape[1]))])
+    return 4.0 * (np.abs(B) @ (np.abs(C) @ (np.abs(Ht) @ (np.abs(D) @ np.abs(A_pad)))))
