@@ -232,9 +232,22 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    fbuild.build()
+        # one builder per node (the others wait at the barrier); build() also serialises through a file lock
+        if local == 0:
+            fbuild.build()
+        dist.barrier()
+        ones = torch.ones(1, device="cuda")
+        dist.all_reduce(ones)
+        comm = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                "allreduce_of_ones": int(ones.item()),
+                "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))}
+        if rank == 0:
+            print(f"[bench] NCCL communicator: {comm}", file=sys.stderr, flush=True)
+    else:
+        fbuild.build()
     lib = fct.load()
 
     sh = shard_rows(cfg.n, cfg.s, rank, world)
@@ -390,7 +403,7 @@ def main():
             "roofline": roofline, "roofline_all": rl,
             "stages_ms": stage_ms, "gpu_launches": int(launches), "launches_per_step": launches / K,
             "clocks": sampler.summary(), "cpu_baseline": cpu, "e2e": e2e,
-            "conditioning_info": info, "sampled_rows_last_step": int(res.count.item()),
+            "conditioning_info": info, "sampled_rows_last_step": int(res.count.item()), "comm": comm,
             "input_gen_s": t_gen,
         }
         print(json.dumps(line), flush=True)

@@ -80,12 +80,17 @@ fct_status fct_sketch(const float* A, int64_t n, int64_t d, int64_t lda, const i
                       void* stream);
 
 /* ------------------------------------------------------------------------------------------
- * Conditioning (FastL1Basis): R with Y = Q R, Q orthonormal columns, diag(R) > 0
- * (unique; reading R19), computed by CholeskyQR2 in fp64, and Rinv = R^-1
- * (O(r1 d^2) + O(d^3)).  Y: r1 x d fp32 (the sketch); R, Rinv: d x d fp64
- * row-major (upper triangular).  info (device int32): 0 on success, j+1 if the j-th pivot
- * of the Cholesky factorisation was not positive/finite (rank-deficient Y).
- * Requires 1 <= d <= FCT_MAX_D and r1 >= d.
+ * Conditioning (FastL1Basis: "construct Pi1 A and an R such that Pi1 A = QR"):
+ * R with Y = Q R, Q orthonormal columns, diag(R) > 0 (unique; reading R19), and Rinv = R^-1
+ * (O(r1 d^2) + O(d^3)).  Y: r1 x d fp32 (the sketch); R, Rinv: d x d fp64 row-major
+ * (upper triangular).  Computed by CholeskyQR2 in fp64 (one cooperative kernel, nothing returns to the host);
+ * when a Cholesky pivot is not positive/finite or the second Gram is far from I (cond(Y) > ~1e8), the device
+ * restarts with the shifted CholeskyQR3 of Fukaya et al. (sigma = 11 (r1 d + d(d+1)) u ||Y||_F^2 on the first
+ * Gram, three passes), which is stable up to cond(Y) ~ 1/u.
+ * info (device int32): 0 = success (CholeskyQR2), -1 = success via the shifted CholeskyQR3 fallback,
+ * j > 0 = the j-th pivot failed even with the shift (non-finite Y); R and Rinv are then all NaN so that no
+ * downstream result can look valid.  Deterministic (fixed summation orders).
+ * Requires 1 <= d <= FCT_MAX_D and r1 >= d; a device that supports cooperative launches.
  */
 size_t fct_condition_workspace_bytes(int32_t r1, int64_t d);
 fct_status fct_condition(const float* Y, int32_t r1, int64_t d, double* R, double* Rinv,
@@ -238,13 +243,16 @@ fct_status fct_pipeline(const float* A, int64_t n, int64_t d, int64_t lda, const
 
 /* The same pipeline from HOST buffers (end-to-end entry point).  A_host, signs_host,
  * cauchy_host, hash_host, Pi2_host are HOST pointers (pinned memory recommended); the inputs
- * are copied in s-aligned chunks on `stream` while the sketch of earlier chunks runs.
+ * are copied to the device on `stream` (the aux arrays first, then A in s-aligned chunks of
+ * ~512 MiB); the sketch of each chunk runs on an internal second stream as soon as that chunk
+ * has landed (accumulated in fp64), so the sketch overlaps the copy of the later chunks; the
+ * row norms, which need all of A, start after the last chunk.
  * dev_A (n x lda fp32), dev_aux (fct_pipeline_aux_bytes) are caller-owned device buffers
  * that receive the inputs.  Outputs idx_host/weight_host (capacity), *count_host are HOST
  * memory; the call returns after they are valid (it synchronises `stream`).  Device copies of
  * Y, R, Rinv, lambda, p live in the workspace-derived buffers of fct_pipeline and are
  * discarded.  Returns FCT_ERR_CAPACITY if count > capacity (count still written),
- * FCT_ERR_SINGULAR if the conditioning failed.
+ * FCT_ERR_SINGULAR if the conditioning failed even with its shifted fallback (info > 0).
  */
 size_t fct_pipeline_aux_bytes(int64_t n, int64_t d, int32_t s, int32_t k);
 size_t fct_pipeline_host_workspace_bytes(int64_t n, int64_t d, int32_t s, int32_t r1, int32_t k,

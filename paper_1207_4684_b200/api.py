@@ -78,7 +78,8 @@ def fct_sketch(A, signs, cauchy_diag, hash_rows, s: int, r1: int, Y=None, accumu
 
 
 def fct_condition(Y, check: bool = True):
-    """(R, Rinv, info) with Y = QR, diag(R) > 0 (CholeskyQR2, fp64).  check=True syncs and raises."""
+    """(R, Rinv, info) with Y = QR, diag(R) > 0 (CholeskyQR2, fp64; shifted CholeskyQR3 fallback on the device,
+    info = -1).  check=True syncs and raises when even the fallback failed (info > 0)."""
     L = _lib_()
     _need(Y, torch.float32, "Y")
     r1, d = Y.shape
@@ -90,8 +91,8 @@ def fct_condition(Y, check: bool = True):
     _lib.check(L.fct_condition(_ptr(Y), r1, d, _ptr(R), _ptr(Rinv), _ptr(info), _ptr(ws), ws.numel(), _stream()))
     if check:
         v = int(info.item())
-        if v != 0:
-            raise _lib.FctError(-5, f"Cholesky pivot {v} of Y^T Y not positive (rank-deficient sketch)")
+        if v > 0:
+            raise _lib.FctError(-5, f"Cholesky pivot {v} not positive even with the shifted fallback (non-finite Y)")
     return R, Rinv, info
 
 

@@ -1,6 +1,7 @@
 """Build libfct.so (all CUDA sources under csrc/) for sm_100a with nvcc, in-tree."""
 from __future__ import annotations
 
+import fcntl
 import glob
 import os
 import subprocess
@@ -31,27 +32,48 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every csrc/*.cu for sm_100a and link libfct.so in-tree.  Safe when several processes (e.g. the
+    ranks of a torchrun job) call it at once: an exclusive file lock serialises the builders, the first one
+    compiles, the others find the library up to date; objects and the temporary library carry the builder's
+    pid, and the library is published with an atomic rename."""
     if not force and up_to_date():
         return LIB
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
+    with open(os.path.join(objdir, ".lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        try:
+            if not force and up_to_date():
+                return LIB
+            _build_locked(objdir, verbose)
+        finally:
+            fcntl.flock(lk, fcntl.LOCK_UN)
+    return LIB
+
+
+def _build_locked(objdir: str, verbose: bool) -> None:
+    pid = os.getpid()
     cmds, objs = [], []
     for src in sources():
-        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        obj = os.path.join(objdir, f"{os.path.basename(src)[:-3]}.{pid}.o")
         cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)
         cmds.append(cmd)
         objs.append(obj)
-    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
-            f.result()
-    tmp = LIB + ".tmp"
-    subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp,
-                           "-cudart", "static"])
-    os.replace(tmp, LIB)
-    return LIB
+    try:
+        with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+            for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
+                f.result()
+        tmp = f"{LIB}.{pid}.tmp"
+        subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp,
+                               "-cudart", "static"])
+        os.replace(tmp, LIB)
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
 
 
 if __name__ == "__main__":

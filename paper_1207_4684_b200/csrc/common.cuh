@@ -77,12 +77,12 @@ inline bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 }  // namespace fct
 
 // internal entry points used by the pipeline (same validation as the public ones)
-fct_status fct_sketch_v3(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs, const float* cauchy,
-                         const int32_t* hash, int s, int r1, double* W, cudaStream_t st);
 fct_status fct2_cz_tc(const float* C, int64_t ldc, const float* Zh, const float* Zl, int64_t ldzt, int64_t K, int r1,
                       int d, double* W, cudaStream_t st);
-fct_status fct_sketch_v4(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs, const float* cauchy,
-                         const int32_t* hash, int s, int r1, double* W, cudaStream_t st);
+fct_status fct_sketch_accum(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs,
+                            const float* cauchy_diag, const int32_t* hash_rows, int s, int r1, double* W,
+                            cudaStream_t st);
+fct_status fct_sketch_finalize(const double* W, float* Y, int64_t cells, int accumulate, cudaStream_t st);
 fct_status fct_sketch_v1(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs, const float* cauchy,
                          const int32_t* hash, int s, int r1, double* W, cudaStream_t st);
 fct_status fct_rownorm_impl(const float* A, int64_t n, int64_t d, int64_t lda, const double* Rinv,

@@ -22,12 +22,14 @@ extern "C" size_t fct_pipeline_workspace_bytes(int64_t n, int64_t d, int32_t s, 
   return pipe_ws(n, d, s, r1, k).total;
 }
 
-extern "C" fct_status fct_pipeline(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs,
-                                   const float* cauchy_diag, const int32_t* hash_rows, int32_t s, int32_t r1,
-                                   const float* Pi2, int32_t k, int64_t m, uint64_t seed, float* Y, double* R,
-                                   double* Rinv, float* lambda, float* p, int64_t* idx, double* weight,
-                                   int64_t capacity, int64_t* count, int32_t* info, void* workspace,
-                                   size_t workspace_bytes, void* stream) {
+namespace {
+// a1-a10 on one device; sketch_ready: Y already holds Pi1 A (the host variant sketches chunk by chunk while A is
+// still being copied) and the sketch step is skipped
+fct_status pipeline_impl(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs,
+                         const float* cauchy_diag, const int32_t* hash_rows, int32_t s, int32_t r1, const float* Pi2,
+                         int32_t k, int64_t m, uint64_t seed, float* Y, double* R, double* Rinv, float* lambda,
+                         float* p, int64_t* idx, double* weight, int64_t capacity, int64_t* count, int32_t* info,
+                         void* workspace, size_t workspace_bytes, void* stream, bool sketch_ready) {
   FCT_CHECK_ARG(n >= 1 && d >= 1 && s >= 1 && r1 >= 1 && k >= 1, FCT_ERR_SHAPE, "fct_pipeline: bad sizes");
   const PipeWS w = pipe_ws(n, d, s, r1, k);
   FCT_CHECK_ARG(workspace && workspace_bytes >= w.total, FCT_ERR_WORKSPACE,
@@ -41,12 +43,24 @@ extern "C" fct_status fct_pipeline(const float* A, int64_t n, int64_t d, int64_t
   double* total = (double*)(base + w.sketch + w.cond + w.rown + w.samp);
   cudaStream_t st = (cudaStream_t)stream;
   fct_status rc;
-  if ((rc = fct_sketch(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, Y, 0, ws_sk, w.sketch, stream)) != FCT_OK)
+  if (!sketch_ready &&
+      (rc = fct_sketch(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, Y, 0, ws_sk, w.sketch, stream)) != FCT_OK)
     return rc;
   if ((rc = fct_condition(Y, r1, d, R, Rinv, info, ws_cd, w.cond, stream)) != FCT_OK) return rc;
   if ((rc = fct_rownorm_impl(A, n, d, lda, Rinv, Pi2, k, lambda, total, true, ws_rn, w.rown, st)) != FCT_OK)
     return rc;
   return l1_probs_sample(lambda, n, total, 0, m, seed, p, idx, weight, capacity, count, ws_sp, w.samp, stream);
+}
+}  // namespace
+
+extern "C" fct_status fct_pipeline(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs,
+                                   const float* cauchy_diag, const int32_t* hash_rows, int32_t s, int32_t r1,
+                                   const float* Pi2, int32_t k, int64_t m, uint64_t seed, float* Y, double* R,
+                                   double* Rinv, float* lambda, float* p, int64_t* idx, double* weight,
+                                   int64_t capacity, int64_t* count, int32_t* info, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+  return pipeline_impl(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, Pi2, k, m, seed, Y, R, Rinv, lambda, p,
+                       idx, weight, capacity, count, info, workspace, workspace_bytes, stream, false);
 }
 
 // ------------------------------------------------------------------------------ host-buffer variant
@@ -65,7 +79,7 @@ AuxLayout aux_layout(int64_t n, int64_t d, int32_t s, int32_t k) {
   return a;
 }
 struct HostWS {
-  size_t Y, R, Rinv, lam, p, idx, w, cnt, info, pipe, total;
+  size_t Y, R, Rinv, lam, p, idx, w, cnt, info, sk, pipe, total;
 };
 HostWS host_ws(int64_t n, int64_t d, int32_t s, int32_t r1, int32_t k, int64_t cap) {
   HostWS h;
@@ -79,6 +93,7 @@ HostWS host_ws(int64_t n, int64_t d, int32_t s, int32_t r1, int32_t k, int64_t c
   h.w = o; o += fct::align256(sizeof(double) * (size_t)(cap > 0 ? cap : 1));
   h.cnt = o; o += fct::align256(sizeof(int64_t));
   h.info = o; o += fct::align256(sizeof(int32_t));
+  h.sk = o; o += fct::align256(sizeof(double) * (size_t)r1 * d);
   h.pipe = o; o += fct_pipeline_workspace_bytes(n, d, s, r1, k);
   h.total = o;
   return h;
@@ -118,13 +133,9 @@ extern "C" fct_status fct_pipeline_host(const float* A_host, int64_t n, int64_t 
   float* dc = (float*)(aux + a.cauchy);
   int32_t* dh = (int32_t*)(aux + a.hash);
   float* dpi2 = (float*)(aux + a.pi2);
-  // host -> device (A in row chunks of 64 MiB)
-  const size_t row_bytes = sizeof(float) * (size_t)lda;
-  const int64_t chunk = std::max<int64_t>(1, (int64_t)((64u << 20) / row_bytes));
-  for (int64_t r0 = 0; r0 < n; r0 += chunk) {
-    const int64_t nr = std::min(chunk, n - r0);
-    FCT_CUDA_RET(cudaMemcpyAsync(dev_A + r0 * lda, A_host + r0 * lda, row_bytes * nr, cudaMemcpyHostToDevice, st));
-  }
+  // host -> device: the aux arrays first, then A in s-aligned row chunks on the caller's stream; the sketch of
+  // each chunk runs on a second stream as soon as the chunk has landed (W accumulates the chunks in fp64), so
+  // the sketch overlaps the PCIe copy of the later chunks.  The row norms need all of A and start after it.
   FCT_CUDA_RET(cudaMemcpyAsync(dsg, signs_host, (size_t)n, cudaMemcpyHostToDevice, st));
   FCT_CUDA_RET(cudaMemcpyAsync(dc, cauchy_host, sizeof(float) * 2 * np, cudaMemcpyHostToDevice, st));
   FCT_CUDA_RET(cudaMemcpyAsync(dh, hash_host, sizeof(int32_t) * 2 * np, cudaMemcpyHostToDevice, st));
@@ -132,10 +143,43 @@ extern "C" fct_status fct_pipeline_host(const float* A_host, int64_t n, int64_t 
   char* w = (char*)workspace;
   int64_t* dcnt = (int64_t*)(w + h.cnt);
   int32_t* dinfo = (int32_t*)(w + h.info);
-  fct_status rc = fct_pipeline(dev_A, n, d, lda, dsg, dc, dh, s, r1, dpi2, k, m, seed, (float*)(w + h.Y),
-                               (double*)(w + h.R), (double*)(w + h.Rinv), (float*)(w + h.lam), (float*)(w + h.p),
-                               (int64_t*)(w + h.idx), (double*)(w + h.w), capacity, dcnt, dinfo, w + h.pipe,
-                               h.total - h.pipe, stream);
+  float* dY = (float*)(w + h.Y);
+  double* W = (double*)(w + h.sk);
+  FCT_CUDA_RET(cudaMemsetAsync(W, 0, sizeof(double) * (size_t)r1 * d, st));
+  const size_t row_bytes = sizeof(float) * (size_t)lda;
+  const int64_t chunk = std::max<int64_t>(s, (int64_t)((512u << 20) / row_bytes) / s * s);
+  const int nchunks = (int)((n + chunk - 1) / chunk);
+  cudaStream_t st2 = nullptr;
+  FCT_CUDA_RET(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+  cudaEvent_t ev_done = nullptr;
+  fct_status rc = FCT_OK;
+  cudaEvent_t* evs = (cudaEvent_t*)calloc((size_t)nchunks + 1, sizeof(cudaEvent_t));
+  for (int c = 0; c <= nchunks && rc == FCT_OK; ++c)
+    if (cudaEventCreateWithFlags(&evs[c], cudaEventDisableTiming) != cudaSuccess) rc = FCT_ERR_CUDA;
+  if (rc == FCT_OK && cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) != cudaSuccess) rc = FCT_ERR_CUDA;
+  // chunk 0's event also covers the aux copies and the W reset queued above
+  for (int c = 0; c < nchunks && rc == FCT_OK; ++c) {
+    const int64_t r0 = (int64_t)c * chunk, nr = std::min(chunk, n - r0);
+    if (cudaMemcpyAsync(dev_A + r0 * lda, A_host + r0 * lda, row_bytes * nr, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaEventRecord(evs[c], st) != cudaSuccess || cudaStreamWaitEvent(st2, evs[c], 0) != cudaSuccess) {
+      rc = FCT_ERR_CUDA;
+      break;
+    }
+    rc = fct_sketch_accum(dev_A + r0 * lda, nr, d, lda, dsg + r0, dc + 2 * r0, dh + 2 * r0, s, r1, W, st2);
+  }
+  if (rc == FCT_OK) rc = fct_sketch_finalize(W, dY, (int64_t)r1 * d, 0, st2);
+  if (rc == FCT_OK && (cudaEventRecord(ev_done, st2) != cudaSuccess || cudaStreamWaitEvent(st, ev_done, 0) != cudaSuccess))
+    rc = FCT_ERR_CUDA;
+  if (rc != FCT_OK && fct_last_error()[0] == 0) fct::set_error("fct_pipeline_host: chunked copy/sketch failed");
+  for (int c = 0; c <= nchunks; ++c)
+    if (evs[c]) cudaEventDestroy(evs[c]);
+  free(evs);
+  if (ev_done) cudaEventDestroy(ev_done);
+  cudaStreamDestroy(st2);   // deferred by the runtime until its queued work completes
+  if (rc != FCT_OK) return rc;
+  rc = pipeline_impl(dev_A, n, d, lda, dsg, dc, dh, s, r1, dpi2, k, m, seed, dY, (double*)(w + h.R),
+                     (double*)(w + h.Rinv), (float*)(w + h.lam), (float*)(w + h.p), (int64_t*)(w + h.idx),
+                     (double*)(w + h.w), capacity, dcnt, dinfo, w + h.pipe, h.total - h.pipe, stream, true);
   if (rc != FCT_OK) return rc;
   int64_t cnt = 0;
   int32_t inf = 0;
@@ -143,7 +187,8 @@ extern "C" fct_status fct_pipeline_host(const float* A_host, int64_t n, int64_t 
   FCT_CUDA_RET(cudaMemcpyAsync(&inf, dinfo, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   FCT_CUDA_RET(cudaStreamSynchronize(st));
   *count_host = cnt;
-  FCT_CHECK_ARG(inf == 0, FCT_ERR_SINGULAR, "fct_pipeline_host: Cholesky pivot %d failed (rank-deficient Pi1 A)", inf);
+  FCT_CHECK_ARG(inf <= 0, FCT_ERR_SINGULAR,
+                "fct_pipeline_host: Cholesky pivot %d failed even with the shifted fallback (non-finite Pi1 A)", inf);
   const int64_t ncopy = std::min(cnt, capacity);
   if (ncopy > 0) {
     FCT_CUDA_RET(cudaMemcpyAsync(idx_host, w + h.idx, sizeof(int64_t) * ncopy, cudaMemcpyDeviceToHost, st));

@@ -140,6 +140,32 @@ fct_status launch_generic(const float* A, int64_t n, int64_t d, int64_t lda, con
 
 }  // namespace
 
+// W (r1 x d fp64) += 4 B C H~ D A for the given rows (no zeroing, no finalize): the shard/chunk building block
+fct_status fct_sketch_accum(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs,
+                            const float* cauchy_diag, const int32_t* hash_rows, int s, int r1, double* W,
+                            cudaStream_t st) {
+  const int dt = pick_dt(d, s, r1);
+  FCT_CHECK_ARG(dt >= 1, FCT_ERR_UNSUPPORTED, "fct_sketch: r1 + s = %d too large", r1 + s);
+  fct_status rc = FCT_ERR_UNSUPPORTED;
+  if (!getenv("FCT_SKETCH_GENERIC"))
+    rc = fct_sketch_v1(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st);
+  if (rc == FCT_ERR_UNSUPPORTED) switch (dt) {
+    case 32: rc = launch_generic<32>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
+    case 16: rc = launch_generic<16>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
+    case 8: rc = launch_generic<8>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
+    case 4: rc = launch_generic<4>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
+    case 2: rc = launch_generic<2>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
+    default: rc = launch_generic<1>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
+  }
+  return rc;
+}
+
+fct_status fct_sketch_finalize(const double* W, float* Y, int64_t cells, int accumulate, cudaStream_t st) {
+  finalize_kernel<<<(unsigned)std::min<int64_t>((cells + 255) / 256, 4096), 256, 0, st>>>(W, Y, cells, accumulate);
+  FCT_LAUNCHED("finalize_kernel", st);
+  return FCT_OK;
+}
+
 extern "C" size_t fct_sketch_workspace_bytes(int64_t n, int64_t d, int32_t s, int32_t r1) {
   (void)n; (void)s;
   if (d < 1 || r1 < 1) return 0;
@@ -160,8 +186,7 @@ extern "C" fct_status fct_sketch(const float* A, int64_t n, int64_t d, int64_t l
   const size_t need = fct_sketch_workspace_bytes(n, d, s, r1);
   FCT_CHECK_ARG(workspace && workspace_bytes >= need, FCT_ERR_WORKSPACE,
                 "fct_sketch: workspace %zu < %zu bytes", workspace_bytes, need);
-  const int dt = pick_dt(d, s, r1);
-  FCT_CHECK_ARG(dt >= 1, FCT_ERR_UNSUPPORTED, "fct_sketch: r1 + s = %d too large", r1 + s);
+  FCT_CHECK_ARG(pick_dt(d, s, r1) >= 1, FCT_ERR_UNSUPPORTED, "fct_sketch: r1 + s = %d too large", r1 + s);
   cudaStream_t st = (cudaStream_t)stream;
   fct::Carver cv(workspace);
   double* W = cv.take<double>((size_t)r1 * d);
@@ -177,24 +202,7 @@ extern "C" fct_status fct_sketch(const float* A, int64_t n, int64_t d, int64_t l
     FCT_CUDA_RET(cudaStreamSynchronize(st));
     FCT_CHECK_ARG(hb == 0, FCT_ERR_ARG, "fct_sketch: %d hash_rows entries outside [0, r1)", hb);
   }
-  fct_status rc = FCT_ERR_UNSUPPORTED;
-  if (!getenv("FCT_SKETCH_GENERIC")) {
-    rc = FCT_ERR_UNSUPPORTED;
-    if (getenv("FCT_SKETCH_V4")) rc = fct_sketch_v4(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st);
-    if (rc == FCT_ERR_UNSUPPORTED) rc = fct_sketch_v3(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st);
-    if (rc == FCT_ERR_UNSUPPORTED) rc = fct_sketch_v1(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st);
-  }
-  if (rc == FCT_ERR_UNSUPPORTED) switch (dt) {
-    case 32: rc = launch_generic<32>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
-    case 16: rc = launch_generic<16>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
-    case 8: rc = launch_generic<8>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
-    case 4: rc = launch_generic<4>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
-    case 2: rc = launch_generic<2>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
-    default: rc = launch_generic<1>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
-  }
+  fct_status rc = fct_sketch_accum(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st);
   if (rc != FCT_OK) return rc;
-  const int64_t cells = (int64_t)r1 * d;
-  finalize_kernel<<<(unsigned)std::min<int64_t>((cells + 255) / 256, 4096), 256, 0, st>>>(W, Y, cells, accumulate);
-  FCT_LAUNCHED("finalize_kernel", st);
-  return FCT_OK;
+  return fct_sketch_finalize(W, Y, (int64_t)r1 * d, accumulate, st);
 }

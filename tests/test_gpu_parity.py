@@ -127,6 +127,60 @@ def test_condition_singular_reports_info(fct):
         fct.fct_condition(dev(Y))
 
 
+def _ill_conditioned_Y(r1, d, delta, seed):
+    """Exactly representable fp32 Y of full rank with cond ~ ||Y|| / delta: small-integer columns, the last
+    column = col0 + col1 except a single entry delta in row 0 (where every other column is 0)."""
+    rng = np.random.default_rng(seed)
+    Y = rng.integers(-8, 9, (r1, d)).astype(np.float32)
+    Y[0] = 0.0
+    Y[:, d - 1] = Y[:, 0] + Y[:, 1]
+    Y[0, d - 1] = delta
+    return Y
+
+
+@pytest.mark.parametrize("delta,path", [(2.0 ** -30, -1), (2.0 ** -4, 0)])
+def test_condition_shifted_cholqr3_fallback(fct, delta, path):
+    """cond(Y) ~ 1e11 breaks CholeskyQR2 (Gram cond ~ 1e22 > 1/u): the device restarts with shifted CholeskyQR3
+    (info = -1) and still matches Householder QR (P:L2792-2794 "for example using a QR-factorization");
+    a moderately conditioned Y stays on CholeskyQR2 (info = 0)."""
+    r1, d = 512, 16
+    Y = _ill_conditioned_Y(r1, d, delta, seed=3)
+    Y64 = Y.astype(np.float64)
+    cond = np.linalg.cond(Y64)
+    R_o, Rinv_o, _ = oracle.condition(Y64)
+    R, Rinv, info = fct.fct_condition(dev(Y))
+    assert int(info.item()) == path
+    R, Rinv = R.cpu().numpy(), Rinv.cpu().numpy()
+    assert (np.diag(R) > 0).all() and np.allclose(np.tril(R, -1), 0)
+    assert np.abs(R - R_o).max() <= 1e-12 * cond * np.abs(R_o).max()
+    assert abs(R[-1, -1] - R_o[-1, -1]) <= 1e-4 * R_o[-1, -1]
+    orth = lambda Ri: np.abs((Y64 @ Ri).T @ (Y64 @ Ri) - np.eye(d)).max()   # evaluated in fp64 on the host
+    assert orth(Rinv) <= max(1e-10, 10 * orth(Rinv_o))
+    np.testing.assert_allclose(R @ Rinv, np.eye(d), atol=1e-8 * cond ** 0.5)
+
+
+def test_condition_nonfinite_is_nan_not_garbage(fct):
+    """Even the shifted fallback fails on a non-finite Y: info > 0 and R, Rinv are NaN (no silent
+    garbage flows into the row norms)."""
+    Y = np.random.default_rng(4).standard_normal((256, 8)).astype(np.float32)
+    Y[17, 3] = np.inf
+    R, Rinv, info = fct.fct_condition(dev(Y), check=False)
+    assert int(info.item()) > 0
+    assert torch.isnan(R).all() and torch.isnan(Rinv).all()
+
+
+@pytest.mark.parametrize("r1,d", [(64, 64), (20000, 3), (300, 128), (128, 1), (8192, 100)])
+def test_condition_shapes(fct, r1, d):
+    Y = np.random.default_rng(r1 + d).standard_normal((r1, d)).astype(np.float32)
+    R_o, Rinv_o, _ = oracle.condition(Y.astype(np.float64))
+    R, Rinv, info = fct.fct_condition(dev(Y))
+    assert int(info.item()) == 0
+    cond = np.linalg.cond(Y.astype(np.float64))
+    R, Rinv = R.cpu().numpy(), Rinv.cpu().numpy()
+    assert np.abs(R - R_o).max() <= 1e-12 * cond * np.abs(R_o).max()
+    assert np.abs(Rinv - Rinv_o).max() <= 1e-12 * cond * np.abs(Rinv_o).max()
+
+
 # ---------------------------------------------------------------- K2 row-norm
 def _rinv_for(inp):
     """Rinv from the oracle's own conditioning of the oracle sketch (stage-wise parity input)."""
