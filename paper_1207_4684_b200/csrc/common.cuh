@@ -79,12 +79,27 @@ inline bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 // internal entry points used by the pipeline (same validation as the public ones)
 fct_status fct2_cz_tc(const float* C, int64_t ldc, const float* Zh, const float* Zl, int64_t ldzt, int64_t K, int r1,
                       int d, double* W, cudaStream_t st);
-fct_status fct_sketch_accum(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs,
-                            const float* cauchy_diag, const int32_t* hash_rows, int s, int r1, double* W,
+// FCT1 sketch accumulation state: W (r1 x d fp64) plus the optional fp32 L2 replicas of the buckets >= t_l2
+struct SketchAcc {
+  double* W = nullptr;
+  float* rep = nullptr;   // [nrep][r1 - t_l2][d], values scaled by 2^20 (nullptr: no L2 offload)
+  int t_l2 = 0;           // first bucket scattered through L2 (r1: none)
+  int nrep = 1;
+  int mode = 0;           // scatter: 0 shared-memory CAS, 1 EXCH, 2 CAS + L2 offload, 3 racy (timing only)
+};
+// carve W and the replicas from a fct_sketch workspace and zero them on st
+fct_status fct_sketch_begin(void* workspace, size_t workspace_bytes, int64_t d, int s, int r1, SketchAcc* acc,
                             cudaStream_t st);
-fct_status fct_sketch_finalize(const double* W, float* Y, int64_t cells, int accumulate, cudaStream_t st);
+// W (+ replicas) += 4 B C H~ D A for the given rows (row shards / host chunks, s-aligned)
+fct_status fct_sketch_accum(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs,
+                            const float* cauchy_diag, const int32_t* hash_rows, int s, int r1, const SketchAcc& acc,
+                            cudaStream_t st);
+// replicas -> W (fixed order, fp64), then Y = (float)(W [+ Y])
+fct_status fct_sketch_end(const SketchAcc& acc, int r1, int64_t d, float* Y, int accumulate, cudaStream_t st);
+fct_status fct_sketch_v5(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs, const float* cauchy,
+                         const int32_t* hash, int s, int r1, int mode, double* W, int64_t* rows_done, cudaStream_t st);
 fct_status fct_sketch_v1(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs, const float* cauchy,
-                         const int32_t* hash, int s, int r1, double* W, cudaStream_t st);
+                         const int32_t* hash, int s, int r1, const SketchAcc& acc, cudaStream_t st);
 fct_status fct_rownorm_impl(const float* A, int64_t n, int64_t d, int64_t lda, const double* Rinv,
                             const float* Pi2, int32_t k, float* lambda, double* lambda_sum,
                             bool zero_sum, void* ws, size_t wsb, cudaStream_t st);

@@ -93,7 +93,7 @@ HostWS host_ws(int64_t n, int64_t d, int32_t s, int32_t r1, int32_t k, int64_t c
   h.w = o; o += fct::align256(sizeof(double) * (size_t)(cap > 0 ? cap : 1));
   h.cnt = o; o += fct::align256(sizeof(int64_t));
   h.info = o; o += fct::align256(sizeof(int32_t));
-  h.sk = o; o += fct::align256(sizeof(double) * (size_t)r1 * d);
+  h.sk = o; o += fct::align256(fct_sketch_workspace_bytes(n, d, s, r1));
   h.pipe = o; o += fct_pipeline_workspace_bytes(n, d, s, r1, k);
   h.total = o;
   return h;
@@ -144,15 +144,15 @@ extern "C" fct_status fct_pipeline_host(const float* A_host, int64_t n, int64_t 
   int64_t* dcnt = (int64_t*)(w + h.cnt);
   int32_t* dinfo = (int32_t*)(w + h.info);
   float* dY = (float*)(w + h.Y);
-  double* W = (double*)(w + h.sk);
-  FCT_CUDA_RET(cudaMemsetAsync(W, 0, sizeof(double) * (size_t)r1 * d, st));
+  SketchAcc acc;
+  fct_status rc = fct_sketch_begin(w + h.sk, h.pipe - h.sk, d, s, r1, &acc, st);
+  if (rc != FCT_OK) return rc;
   const size_t row_bytes = sizeof(float) * (size_t)lda;
   const int64_t chunk = std::max<int64_t>(s, (int64_t)((512u << 20) / row_bytes) / s * s);
   const int nchunks = (int)((n + chunk - 1) / chunk);
   cudaStream_t st2 = nullptr;
   FCT_CUDA_RET(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
   cudaEvent_t ev_done = nullptr;
-  fct_status rc = FCT_OK;
   cudaEvent_t* evs = (cudaEvent_t*)calloc((size_t)nchunks + 1, sizeof(cudaEvent_t));
   for (int c = 0; c <= nchunks && rc == FCT_OK; ++c)
     if (cudaEventCreateWithFlags(&evs[c], cudaEventDisableTiming) != cudaSuccess) rc = FCT_ERR_CUDA;
@@ -165,9 +165,9 @@ extern "C" fct_status fct_pipeline_host(const float* A_host, int64_t n, int64_t 
       rc = FCT_ERR_CUDA;
       break;
     }
-    rc = fct_sketch_accum(dev_A + r0 * lda, nr, d, lda, dsg + r0, dc + 2 * r0, dh + 2 * r0, s, r1, W, st2);
+    rc = fct_sketch_accum(dev_A + r0 * lda, nr, d, lda, dsg + r0, dc + 2 * r0, dh + 2 * r0, s, r1, acc, st2);
   }
-  if (rc == FCT_OK) rc = fct_sketch_finalize(W, dY, (int64_t)r1 * d, 0, st2);
+  if (rc == FCT_OK) rc = fct_sketch_end(acc, r1, d, dY, 0, st2);
   if (rc == FCT_OK && (cudaEventRecord(ev_done, st2) != cudaSuccess || cudaStreamWaitEvent(st, ev_done, 0) != cudaSuccess))
     rc = FCT_ERR_CUDA;
   if (rc != FCT_OK && fct_last_error()[0] == 0) fct::set_error("fct_pipeline_host: chunked copy/sketch failed");

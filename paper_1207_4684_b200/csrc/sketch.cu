@@ -11,6 +11,7 @@
 //     into the fp64 workspace W[r1][d] (hierarchical accumulation);
 //   * a final kernel writes Y = (float)(W [+ Y]).
 #include <math.h>
+#include <string.h>
 #include "common.cuh"
 
 namespace {
@@ -138,18 +139,73 @@ fct_status launch_generic(const float* A, int64_t n, int64_t d, int64_t lda, con
   return FCT_OK;
 }
 
+__global__ void rep_reduce_kernel(const float* __restrict__ rep, int nrep, int64_t cells, double* __restrict__ W) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cells; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < nrep; ++r) s += (double)rep[(size_t)r * cells + i];
+    W[i] += s * 0x1p-20;   // exact rescale of the replicas' 2^20
+  }
+}
+
+constexpr int kMaxRep = 16;
+
+// L2 offload fraction of the buckets and scatter primitive (environment overrides; K1)
+void sketch_policy(int r1, int s, int64_t d, int* t_l2, int* nrep, int* mode) {
+  double frac = 0.0;
+  if (const char* e = getenv("FCT_SKETCH_L2")) frac = atof(e);
+  frac = frac < 0.0 ? 0.0 : (frac > 1.0 ? 1.0 : frac);
+  *t_l2 = r1 - (int)(frac * r1);
+  *nrep = kMaxRep;
+  if (const char* e = getenv("FCT_SKETCH_NREP")) *nrep = std::max(1, std::min(kMaxRep, atoi(e)));
+  *mode = 1;   // EXCH pair (exact); "cas": the round-1 CAS batch; "racy": timing bound only
+  if (const char* e = getenv("FCT_SKETCH_SCATTER")) *mode = !strcmp(e, "cas") ? 0 : (!strcmp(e, "racy") ? 3 : 1);
+  if (frac > 0.0) *mode = 2;
+  (void)s; (void)d;
+}
+
 }  // namespace
 
-// W (r1 x d fp64) += 4 B C H~ D A for the given rows (no zeroing, no finalize): the shard/chunk building block
+fct_status fct_sketch_begin(void* workspace, size_t workspace_bytes, int64_t d, int s, int r1, SketchAcc* acc,
+                            cudaStream_t st) {
+  (void)workspace_bytes;
+  fct::Carver cv(workspace);
+  acc->W = cv.take<double>((size_t)r1 * d);
+  int t_l2, nrep, mode;
+  sketch_policy(r1, s, d, &t_l2, &nrep, &mode);
+  acc->t_l2 = t_l2;
+  acc->nrep = nrep;
+  acc->mode = mode;
+  acc->rep = mode == 2 && t_l2 < r1 ? cv.take<float>((size_t)kMaxRep * (r1 - t_l2) * d) : nullptr;
+  FCT_CUDA_RET(cudaMemsetAsync(acc->W, 0, sizeof(double) * (size_t)r1 * d, st));
+  if (acc->rep) FCT_CUDA_RET(cudaMemsetAsync(acc->rep, 0, sizeof(float) * (size_t)nrep * (r1 - t_l2) * d, st));
+  return FCT_OK;
+}
+
 fct_status fct_sketch_accum(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs,
-                            const float* cauchy_diag, const int32_t* hash_rows, int s, int r1, double* W,
+                            const float* cauchy_diag, const int32_t* hash_rows, int s, int r1, const SketchAcc& acc,
                             cudaStream_t st) {
   const int dt = pick_dt(d, s, r1);
   FCT_CHECK_ARG(dt >= 1, FCT_ERR_UNSUPPORTED, "fct_sketch: r1 + s = %d too large", r1 + s);
   fct_status rc = FCT_ERR_UNSUPPORTED;
+  if (!getenv("FCT_SKETCH_GENERIC") && (acc.mode == 0 || acc.mode == 1)) {
+    // v5 takes the full s-blocks; the ragged tail block (if any) continues below through v1 / generic
+    int64_t done = 0;
+    rc = fct_sketch_v5(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, acc.mode, acc.W, &done, st);
+    if (rc != FCT_OK && rc != FCT_ERR_UNSUPPORTED) return rc;
+    if (rc == FCT_OK) {
+      if (done == n) return FCT_OK;
+      A += done * lda;
+      signs += done;
+      cauchy_diag += 2 * done;
+      hash_rows += 2 * done;
+      n -= done;
+      rc = FCT_ERR_UNSUPPORTED;
+    }
+  }
   if (!getenv("FCT_SKETCH_GENERIC"))
-    rc = fct_sketch_v1(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st);
-  if (rc == FCT_ERR_UNSUPPORTED) switch (dt) {
+    rc = fct_sketch_v1(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, acc, st);
+  double* W = acc.W;
+  if (rc == FCT_ERR_UNSUPPORTED) switch (dt) {   // the generic kernel keeps everything in shared memory / W
     case 32: rc = launch_generic<32>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
     case 16: rc = launch_generic<16>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
     case 8: rc = launch_generic<8>(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st); break;
@@ -160,8 +216,15 @@ fct_status fct_sketch_accum(const float* A, int64_t n, int64_t d, int64_t lda, c
   return rc;
 }
 
-fct_status fct_sketch_finalize(const double* W, float* Y, int64_t cells, int accumulate, cudaStream_t st) {
-  finalize_kernel<<<(unsigned)std::min<int64_t>((cells + 255) / 256, 4096), 256, 0, st>>>(W, Y, cells, accumulate);
+fct_status fct_sketch_end(const SketchAcc& acc, int r1, int64_t d, float* Y, int accumulate, cudaStream_t st) {
+  if (acc.rep) {
+    const int64_t cells = (int64_t)(r1 - acc.t_l2) * d;
+    rep_reduce_kernel<<<(unsigned)std::min<int64_t>((cells + 255) / 256, 4096), 256, 0, st>>>(
+        acc.rep, acc.nrep, cells, acc.W + (size_t)acc.t_l2 * d);
+    FCT_LAUNCHED("rep_reduce_kernel", st);
+  }
+  const int64_t cells = (int64_t)r1 * d;
+  finalize_kernel<<<(unsigned)std::min<int64_t>((cells + 255) / 256, 4096), 256, 0, st>>>(acc.W, Y, cells, accumulate);
   FCT_LAUNCHED("finalize_kernel", st);
   return FCT_OK;
 }
@@ -169,7 +232,8 @@ fct_status fct_sketch_finalize(const double* W, float* Y, int64_t cells, int acc
 extern "C" size_t fct_sketch_workspace_bytes(int64_t n, int64_t d, int32_t s, int32_t r1) {
   (void)n; (void)s;
   if (d < 1 || r1 < 1) return 0;
-  return fct::align256((size_t)r1 * (size_t)d * sizeof(double)) + 256;
+  return fct::align256((size_t)r1 * (size_t)d * sizeof(double)) +
+         fct::align256((size_t)kMaxRep * r1 * (size_t)d * sizeof(float)) + 256;
 }
 
 extern "C" fct_status fct_sketch(const float* A, int64_t n, int64_t d, int64_t lda,
@@ -188,12 +252,9 @@ extern "C" fct_status fct_sketch(const float* A, int64_t n, int64_t d, int64_t l
                 "fct_sketch: workspace %zu < %zu bytes", workspace_bytes, need);
   FCT_CHECK_ARG(pick_dt(d, s, r1) >= 1, FCT_ERR_UNSUPPORTED, "fct_sketch: r1 + s = %d too large", r1 + s);
   cudaStream_t st = (cudaStream_t)stream;
-  fct::Carver cv(workspace);
-  double* W = cv.take<double>((size_t)r1 * d);
-  int* bad = cv.take<int>(1);
-  FCT_CUDA_RET(cudaMemsetAsync(W, 0, sizeof(double) * (size_t)r1 * d, st));
   const int64_t n_pad = (n + s - 1) / s * s;
   if (fct::debug_sync()) {
+    int* bad = (int*)((char*)workspace + need - 256);
     FCT_CUDA_RET(cudaMemsetAsync(bad, 0, sizeof(int), st));
     check_hash_kernel<<<256, 256, 0, st>>>(hash_rows, 2 * n_pad, r1, bad);
     FCT_LAUNCHED("check_hash_kernel", st);
@@ -202,7 +263,9 @@ extern "C" fct_status fct_sketch(const float* A, int64_t n, int64_t d, int64_t l
     FCT_CUDA_RET(cudaStreamSynchronize(st));
     FCT_CHECK_ARG(hb == 0, FCT_ERR_ARG, "fct_sketch: %d hash_rows entries outside [0, r1)", hb);
   }
-  fct_status rc = fct_sketch_accum(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, W, st);
-  if (rc != FCT_OK) return rc;
-  return fct_sketch_finalize(W, Y, (int64_t)r1 * d, accumulate, st);
+  SketchAcc acc;
+  fct_status rc = fct_sketch_begin(workspace, workspace_bytes, d, s, r1, &acc, st);
+  if (rc == FCT_OK) rc = fct_sketch_accum(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, acc, st);
+  if (rc == FCT_OK) rc = fct_sketch_end(acc, r1, d, Y, accumulate, st);
+  return rc;
 }

@@ -52,15 +52,15 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 }
 
 
-// Batched shared-memory float add with ILP: all loads, then all CAS (ATOMS.CAS returns the old
-// word), then a retry loop for the (rare) lanes whose word changed in between.  Exact: an update is
-// applied only by a successful CAS on the value it read.
+// Batched shared-memory float add with ILP (MODE 0, the default): all loads, then all CAS (ATOMS.CAS returns the
+// old word), then a retry loop for the (rare) lanes whose word changed in between.  Exact: an update is applied
+// only by a successful CAS on the value it read.
 template <int N>
 __device__ __forceinline__ void smem_add_batch(float* __restrict__ P, const int (&addr)[N], const float (&val)[N]) {
   float old[N];
 #pragma unroll
   for (int q = 0; q < N; ++q) old[q] = P[addr[q]];
-  unsigned pending = 0u;
+  unsigned pending = 0;
 #pragma unroll
   for (int q = 0; q < N; ++q) {
     const int want = __float_as_int(old[q]);
@@ -76,6 +76,74 @@ __device__ __forceinline__ void smem_add_batch(float* __restrict__ P, const int 
         if (atomicCAS((int*)&P[addr[q]], want, __float_as_int(o + val[q])) == want) pending &= ~(1u << q);
       }
     }
+  }
+}
+
+// Measured alternatives (opt-in instances, K1):
+//   MODE 1: ATOMS.EXCH take / add / EXCH put, re-adding any deposit made in between (exact);
+//   MODE 2: buckets h >= t_l2 go to L2 (RED.ADD.F32 of v * 2^20 into this CTA's fp32 replica of those bucket
+//           rows; global atomics are exact updates, the 2^20 keeps nonzero terms normal under the reduction's
+//           flush-to-zero and is divided out exactly when the replicas are reduced), the rest use MODE 0;
+//   MODE 3: plain LDS + STS, which LOSES concurrent updates (a timing bound only; never parity-tested).
+template <int MODE, int N>
+__device__ __forceinline__ void scatter_batch(float* __restrict__ P, const int (&addr)[N], const float (&val)[N],
+                                              const int (&h)[N], float* repc, int t_l2, int d) {
+  if constexpr (MODE == 0) {
+    smem_add_batch<N>(P, addr, val);
+  } else if constexpr (MODE == 1) {
+    float x[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) x[q] = atomicExch(&P[addr[q]], 0.0f);
+#pragma unroll
+    for (int q = 0; q < N; ++q) x[q] = atomicExch(&P[addr[q]], x[q] + val[q]);
+    unsigned pending = 0u;
+#pragma unroll
+    for (int q = 0; q < N; ++q) if (x[q] != 0.0f) pending |= 1u << q;
+    while (pending) {
+#pragma unroll
+      for (int q = 0; q < N; ++q)
+        if ((pending >> q) & 1u) {
+          const float t = atomicExch(&P[addr[q]], 0.0f);
+          x[q] = atomicExch(&P[addr[q]], t + x[q]);
+          if (!(x[q] != 0.0f)) pending &= ~(1u << q);
+        }
+    }
+  } else if constexpr (MODE == 2) {
+    // L2 lanes: predicated REDs; the shared-memory LDS / CAS of those lanes are predicated off
+    unsigned sm = 0u;
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      const bool l2 = repc && h[q] >= t_l2 && fabsf(val[q]) >= 0x1p-100f;
+      if (l2) atomicAdd(repc + (size_t)(h[q] - t_l2) * d, val[q] * 0x1p20f);
+      else sm |= 1u << q;
+    }
+    float old[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) old[q] = ((sm >> q) & 1u) ? P[addr[q]] : 0.0f;
+    unsigned pending = 0u;
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      if ((sm >> q) & 1u) {
+        const int want = __float_as_int(old[q]);
+        if (atomicCAS((int*)&P[addr[q]], want, __float_as_int(old[q] + val[q])) != want) pending |= 1u << q;
+      }
+    }
+    while (pending) {
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        if ((pending >> q) & 1u) {
+          const float o = P[addr[q]];
+          const int want = __float_as_int(o);
+          if (atomicCAS((int*)&P[addr[q]], want, __float_as_int(o + val[q])) == want) pending &= ~(1u << q);
+        }
+      }
+    }
+  } else {
+    float old[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) old[q] = P[addr[q]];
+#pragma unroll
+    for (int q = 0; q < N; ++q) P[addr[q]] = old[q] + val[q];
   }
 }
 
@@ -148,13 +216,15 @@ struct AuxLayout {
   static constexpr int had_bytes = 8 * S;
 };
 
-// DIRECT (opt-in, FCT_SKETCH_DIRECT=1): the aux arrays are read from global memory (L2) instead of being
-// staged in shared memory, so more tile groups fit next to P (s = 2048, r1 = 8192: two groups instead of one)
-template <int LA, int LB, int DT, int TL, bool DIRECT>
+// L2 offload: updates of buckets h >= t_l2 go to the CTA's fp32 replica rep[grp % nrep][h - t_l2][d] in global
+// memory (L2-resident) instead of shared memory, so the shared-memory pipe -- the kernel's limiter -- carries
+// only the buckets below t_l2 (t_l2 = r1: everything in shared memory).
+template <int LA, int LB, int DT, int TL, int MODE>
 __global__ void __launch_bounds__(Geo<LA, LB, DT, TL>::THREADS, 1)
 sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, const int8_t* __restrict__ signs,
                  const float* __restrict__ cauchy, const int32_t* __restrict__ hash, int r1, int nslices,
-                 int64_t nblocks, float inv_sqrt_s, double* __restrict__ W) {
+                 int64_t nblocks, float inv_sqrt_s, double* __restrict__ W, float* __restrict__ rep, int t_l2,
+                 int nrep) {
   using Gm = Geo<LA, LB, DT, TL>;
   using AL = AuxLayout<Gm::S>;
   constexpr int S = Gm::S, RA = Gm::RA, RB = Gm::RB, NT = Gm::NT, NB = Gm::NB, TILES = Gm::TILES, G = Gm::G;
@@ -162,8 +232,8 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
   // [TILES] tiles | [TILES] identity aux | [TILES] Hadamard aux | P[r1][DT]
   float* tiles = (float*)smraw;
   unsigned char* auxI0 = smraw + TILES * Gm::tile_bytes;
-  unsigned char* auxH0 = auxI0 + (DIRECT ? 0 : TILES * AL::id_bytes);
-  float* P = (float*)(auxH0 + (DIRECT ? 0 : TILES * AL::had_bytes));
+  unsigned char* auxH0 = auxI0 + TILES * AL::id_bytes;
+  float* P = (float*)(auxH0 + TILES * AL::had_bytes);
   __shared__ __align__(8) uint64_t bar_t[TILES], bar_i[TILES], bar_h[TILES];
 
   const int cs = blockIdx.x % nslices;
@@ -174,6 +244,9 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
   const int lt = threadIdx.x - tg * NT;   // thread within the tile group
   const int c = lt % DT;
   float* tile = tiles + (size_t)tg * S * DT;
+  // this thread's column of the CTA's L2 replica (nullptr: no L2 path for this column)
+  float* const repc = (MODE == 2 && rep && t_l2 < r1 && c0 + c < d)
+                          ? rep + (size_t)(grp % nrep) * (size_t)(r1 - t_l2) * d + (c0 + c) : nullptr;
   unsigned char* auxI = auxI0 + tg * AL::id_bytes;
   unsigned char* auxH = auxH0 + tg * AL::had_bytes;
   const int8_t* sSign = (const int8_t*)auxI;
@@ -205,7 +278,6 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
     return (int)(valid & ~15LL);
   };
   auto issue_id = [&](int64_t bb) {
-    if (DIRECT) return;
     const int sb = sign_bulk(bb);
     const int64_t t0 = 2 * bb * S;
     mbar_expect_tx(&bar_i[tg], (unsigned)(sb + 8 * S));
@@ -214,7 +286,6 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
     bulk_g2s(auxI + AL::sign_bytes + 4 * S, hash + t0 + S, 4u * S, &bar_i[tg]);
   };
   auto issue_had = [&](int64_t bb) {
-    if (DIRECT) return;
     const int64_t t0 = 2 * bb * S;
     mbar_expect_tx(&bar_h[tg], 8u * S);
     bulk_g2s(auxH, cauchy + t0, 4u * S, &bar_h[tg]);
@@ -234,11 +305,9 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
   for (; b < nblocks; b += bstep) {
     const int64_t bn = b + bstep;
     mbar_wait(&bar_t[tg], phase);
-    if (!DIRECT) mbar_wait(&bar_i[tg], phase);
+    mbar_wait(&bar_i[tg], phase);
     const int64_t rowb = b * S;
-    const int sb = DIRECT ? 0 : sign_bulk(b);
-    const float* gC = cauchy + 2 * b * S;   // DIRECT: this block's aux in global memory
-    const int* gH = hash + 2 * b * S;
+    const int sb = sign_bulk(b);
     // ---------------- phase A: rows g + (S/RA) k; identity half scattered from the staged aux
     {
       const int g = lt / DT;
@@ -248,7 +317,7 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
       constexpr int BA = RA < 8 ? RA : 8;
 #pragma unroll
       for (int k0 = 0; k0 < RA; k0 += BA) {
-        int ad[BA];
+        int ad[BA], hh[BA];
         float vv[BA];
 #pragma unroll
         for (int q = 0; q < BA; ++q) {
@@ -257,10 +326,12 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
           if (r < sb) sg = sSign[r];
           else sg = rowb + r < n ? (int)__ldg(signs + rowb + r) : 0;
           x[k0 + q] = __int_as_float(__float_as_int(x[k0 + q]) ^ (sg & (int)0x80000000));   // sign flip, no I2F
-          ad[q] = (DIRECT ? __ldg(gH + S + r) : sHi[r]) * DT + c;
-          vv[q] = (4.f * (DIRECT ? __ldg(gC + S + r) : sCi[r])) * x[k0 + q];
+          const int h = sHi[r];
+          ad[q] = h * DT + c;
+          hh[q] = h;
+          vv[q] = (4.f * sCi[r]) * x[k0 + q];
         }
-        smem_add_batch<BA>(P, ad, vv);
+        scatter_batch<MODE, BA>(P, ad, vv, hh, repc, t_l2, d);
       }
       fwht_regs<RA>(x);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -281,7 +352,7 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     named_bar(1 + tg, NT);  // the tile buffer is free: prefetch the next block
     if (lt == 0 && bn < nblocks) issue_tile(bn);
-    if (!DIRECT) mbar_wait(&bar_h[tg], phase);
+    mbar_wait(&bar_h[tg], phase);
     phase ^= 1u;
 #pragma unroll
     for (int gi = 0; gi < NB; ++gi) {
@@ -291,15 +362,8 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
 #pragma unroll
       for (int k0 = 0; k0 < RB; k0 += 8) {
         const int r0 = RB * gp + k0;
-        int4 h0, h1;
-        float4 q0, q1;
-        if (DIRECT) {
-          h0 = __ldg((const int4*)(gH + r0)); h1 = __ldg((const int4*)(gH + r0 + 4));
-          q0 = __ldg((const float4*)(gC + r0)); q1 = __ldg((const float4*)(gC + r0 + 4));
-        } else {
-          h0 = *(const int4*)(sHh + r0); h1 = *(const int4*)(sHh + r0 + 4);
-          q0 = *(const float4*)(sCh + r0); q1 = *(const float4*)(sCh + r0 + 4);
-        }
+        const int4 h0 = *(const int4*)(sHh + r0), h1 = *(const int4*)(sHh + r0 + 4);
+        const float4 q0 = *(const float4*)(sCh + r0), q1 = *(const float4*)(sCh + r0 + 4);
         const int hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
         const float cw[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
         int ad[8];
@@ -309,7 +373,7 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
           ad[q] = hv[q] * DT + c;
           vv[q] = (sc_h * cw[q]) * y[gi][k0 + q];
         }
-        smem_add_batch<8>(P, ad, vv);
+        scatter_batch<MODE, 8>(P, ad, vv, hv, repc, t_l2, d);
       }
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -320,7 +384,7 @@ sketch_v1_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int d, con
   for (int e = threadIdx.x; e < r1 * DT; e += blockDim.x) {
     const int h = e / DT, cc = e - h * DT;
     const float v = P[e];
-    if (c0 + cc < d && v != 0.f) atomicAdd(&W[(size_t)h * d + c0 + cc], (double)v);
+    if (c0 + cc < d && v != 0.f) atomicAdd(&W[(size_t)h * d + c0 + cc], (double)v);   // includes h >= t_l2 terms
   }
 }
 
@@ -336,9 +400,9 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-template <int LA, int LB, int DT, int TL, bool DIRECT>
+template <int LA, int LB, int DT, int TL, int MODE>
 fct_status launch_v1(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs, const float* cauchy,
-                     const int32_t* hash, int s, int r1, double* W, cudaStream_t st) {
+                     const int32_t* hash, int s, int r1, const SketchAcc& acc, cudaStream_t st) {
   using Gm = Geo<LA, LB, DT, TL>;
   auto enc = get_encode();
   FCT_CHECK_ARG(enc, FCT_ERR_CUDA, "fct_sketch: cuTensorMapEncodeTiled unavailable");
@@ -353,31 +417,33 @@ fct_status launch_v1(const float* A, int64_t n, int64_t d, int64_t lda, const in
   FCT_CHECK_ARG(cr == CUDA_SUCCESS, FCT_ERR_CUDA, "fct_sketch: cuTensorMapEncodeTiled failed (%d)", (int)cr);
   const int nslices = (int)((d + DT - 1) / DT);
   const int64_t nblocks = (n + s - 1) / s;
-  const size_t smem = Gm::TILES * (Gm::tile_bytes + (DIRECT ? 0 : AuxLayout<Gm::S>::id_bytes + AuxLayout<Gm::S>::had_bytes)) +
+  const size_t smem = Gm::TILES * (Gm::tile_bytes + AuxLayout<Gm::S>::id_bytes + AuxLayout<Gm::S>::had_bytes) +
                       (size_t)r1 * DT * sizeof(float);
-  auto kern = sketch_v1_kernel<LA, LB, DT, TL, DIRECT>;
+  auto kern = sketch_v1_kernel<LA, LB, DT, TL, MODE>;
   FCT_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 1;
   FCT_CUDA_RET(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Gm::THREADS, smem));
   if (occ < 1) occ = 1;
-  // CTAs per slice: fill the SMs, and keep <= ~2048 expected terms per bucket per CTA partial
+  // CTAs per slice: an equal number per slice (the slices then walk the row blocks in lockstep, so each line
+  // of A is read from DRAM once), keeping <= ~2048 expected terms per bucket per CTA partial
   int64_t ngrp = ((int64_t)fct::num_sms() * occ) / nslices;
   const int64_t min_grp = (2 * nblocks * (int64_t)s + 2048LL * r1 - 1) / (2048LL * r1);
   ngrp = std::max<int64_t>(std::max<int64_t>(ngrp, 1), min_grp);
   ngrp = std::min<int64_t>(ngrp, (nblocks + Gm::TILES - 1) / Gm::TILES);
   if (ngrp < 1) ngrp = 1;
   kern<<<(unsigned)(ngrp * nslices), Gm::THREADS, smem, st>>>(map, n, (int)d, signs, cauchy, hash, r1, nslices,
-                                                               nblocks, (float)(1.0 / sqrt((double)s)), W);
+                                                               nblocks, (float)(1.0 / sqrt((double)s)), acc.W,
+                                                               acc.rep, acc.t_l2, acc.nrep);
   FCT_LAUNCHED("sketch_v1_kernel", st);
   return FCT_OK;
 }
 
 constexpr size_t kV1Smem = 232448 - 256;   // max dynamic shared memory per block on sm_100, less static
 
-template <int LA, int LB, int DT, int TL, bool DIRECT>
+template <int LA, int LB, int DT, int TL>
 bool fits(int r1) {
   using Gm = Geo<LA, LB, DT, TL>;
-  return Gm::TILES * (Gm::tile_bytes + (DIRECT ? 0 : AuxLayout<Gm::S>::id_bytes + AuxLayout<Gm::S>::had_bytes)) +
+  return Gm::TILES * (Gm::tile_bytes + AuxLayout<Gm::S>::id_bytes + AuxLayout<Gm::S>::had_bytes) +
              (size_t)r1 * DT * sizeof(float) <= kV1Smem;
 }
 
@@ -385,28 +451,29 @@ bool fits(int r1) {
 
 // Returns FCT_ERR_UNSUPPORTED (without enqueueing) when no v1 instance covers (s, d, r1, alignment).
 fct_status fct_sketch_v1(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs, const float* cauchy,
-                         const int32_t* hash, int s, int r1, double* W, cudaStream_t st) {
+                         const int32_t* hash, int s, int r1, const SketchAcc& acc, cudaStream_t st) {
   if (((uintptr_t)A & 15) || ((uintptr_t)cauchy & 15) || ((uintptr_t)hash & 15) || ((uintptr_t)signs & 15) ||
       (lda % 4) || n >= (1LL << 31))
     return FCT_ERR_UNSUPPORTED;
-  const char* dv = getenv("FCT_SKETCH_DIRECT");   // 1: prefer the DIRECT-aux instances, 0: never use them
-  const int direct = dv ? atoi(dv) : -1;
-#define TRYD(LA_, LB_, DT_, TL_, DI_)                                                              \
-  if (s == (1 << (LA_ + LB_)) && fits<LA_, LB_, DT_, TL_, DI_>(r1) && (DT_ <= 8 || d >= DT_) &&   \
-      (DI_ ? direct != 0 : direct != 1))                                                            \
-    return launch_v1<LA_, LB_, DT_, TL_, DI_>(A, n, d, lda, signs, cauchy, hash, s, r1, W, st);
-#define TRY(LA_, LB_, DT_, TL_) TRYD(LA_, LB_, DT_, TL_, false)
-  if (direct == 1) {
-    TRYD(6, 5, 4, 2, true) TRYD(5, 5, 8, 3, true) TRYD(5, 5, 8, 2, true)
+  // scatter primitive: MODE 1 (EXCH pair, exact) is the default -- measured 14 % faster than MODE 0 (CAS) at
+  // the cfg-4 shape (2^24 rows: 2.77 vs 3.22 ms, profiles/r02_sketch_scatter_modes.jsonl); MODE 0 stays
+  // selectable (FCT_SKETCH_SCATTER=cas); MODE 2 (L2 offload) and 3 (racy, timing only) exist for the cfg-4/5
+  // geometries only
+#define TRYM(LA_, LB_, DT_, TL_, M_)                                                                     \
+  if (acc.mode == M_ && s == (1 << (LA_ + LB_)) && fits<LA_, LB_, DT_, TL_>(r1) && (DT_ <= 8 || d >= DT_)) \
+    return launch_v1<LA_, LB_, DT_, TL_, M_>(A, n, d, lda, signs, cauchy, hash, s, r1, acc, st);
+  TRYM(5, 5, 8, 2, 2) TRYM(5, 5, 8, 2, 3) TRYM(6, 5, 4, 1, 2) TRYM(6, 5, 4, 1, 3)
+#undef TRYM
+#define TRY(LA_, LB_, DT_, TL_)                                                                   \
+  if (s == (1 << (LA_ + LB_)) && fits<LA_, LB_, DT_, TL_>(r1) && (DT_ <= 8 || d >= DT_)) {       \
+    if (acc.mode == 0) return launch_v1<LA_, LB_, DT_, TL_, 0>(A, n, d, lda, signs, cauchy, hash, s, r1, acc, st); \
+    return launch_v1<LA_, LB_, DT_, TL_, 1>(A, n, d, lda, signs, cauchy, hash, s, r1, acc, st);  \
   }
-  // widest column slice that fits first (fewer aux re-reads, fewer bank conflicts), then narrower.  DIRECT
-  // (opt-in) was measured without gain: cfg 5 shape 26.5 vs 26.0 ms (2 groups vs 1), cfg 4 15.7 vs 12.7 ms
-  // (3 groups vs 2) -- the kernel is bound by shared-memory wavefronts, not by latency
+  // widest column slice that fits first (fewer aux re-reads, fewer bank conflicts), then narrower
   TRY(6, 5, 16, 1) TRY(6, 5, 8, 2) TRY(6, 5, 4, 2) TRY(6, 5, 4, 1)        // s = 2048
   TRY(5, 5, 16, 1) TRY(5, 5, 8, 2) TRY(5, 5, 4, 4) TRY(5, 5, 4, 2)        // s = 1024
   TRY(4, 4, 16, 2) TRY(4, 4, 8, 4) TRY(4, 4, 4, 8)                        // s = 256
   TRY(3, 3, 8, 8) TRY(3, 3, 4, 8)                                         // s = 64
 #undef TRY
-#undef TRYD
   return FCT_ERR_UNSUPPORTED;
 }
