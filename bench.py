@@ -13,6 +13,7 @@ Prints ONE JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -38,30 +39,51 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic(cfg, n_loc, world):
+TRAFFIC_FILE = os.path.join("profiles", "r02_ncu_full_cfg4_traffic.json")
+
+
+def load_traffic(cfg, n_loc, world, instances=None):
     """DRAM bytes per launch (read + write) of each kernel from the committed ncu --set full capture of this
-    exact workload (profiles/r01_ncu_full_cfg4_traffic.json); {} when the capture does not match."""
-    p = os.path.join(ROOT, "profiles", "r01_ncu_full_cfg4_traffic.json")
+    exact workload, plus its measured limiter; {} when the capture's workload or its KERNEL INSTANCES differ from
+    the ones this run launched (instances: {"fct1_sketch": "sketch_v5_kernel<...>", "l1_rownorm": "..."})."""
+    p = os.path.join(ROOT, TRAFFIC_FILE)
     try:
         with open(p) as f:
             m = json.load(f)
         w = m["workload"]
         if world != 1 or cfg.idx != w["config"] or n_loc != w["n"] or cfg.d != w["d"]:
             return {}
-        out = {k: v["dram_bytes_read"] + v["dram_bytes_write"] for k, v in m["kernels"].items()}
-        out["_source"] = "profiles/r01_ncu_full_cfg4_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum)"
-        sk = m["kernels"].get("fct1_sketch", {})
-        if "smem_pipe_pct_of_peak" in sk:
-            # the sketch's measured limiter is the shared-memory data pipe, not DRAM (DESIGN.md K1)
-            out["_limiter"] = {"fct1_sketch": {
-                "resource": "shared-memory data pipe (l1tex lsu wavefronts, 1 per cycle per SM)",
-                "pct_of_peak": sk["smem_pipe_pct_of_peak"],
-                "wavefronts_per_launch": sk["smem_wavefronts"],
-                "source": "profiles/r01_ncu_full_cfg4_traffic.json (l1tex__data_pipe_lsu_wavefronts_mem_shared.sum / "
-                          "(sm__cycles_elapsed.avg x 148))"}}
+        out = {}
+        for k, v in m["kernels"].items():
+            launched = (instances or {}).get(k)
+            if launched is None or launched not in v["kernel"]:
+                out.setdefault("_mismatch", {})[k] = {"captured": v["kernel"], "launched": launched}
+                continue
+            out[k] = v["dram_bytes_read"] + v["dram_bytes_write"]
+            if v.get("limiter"):
+                out.setdefault("_limiter", {})[k] = dict(v["limiter"], source=TRAFFIC_FILE)
+        out["_source"] = TRAFFIC_FILE + " (dram__bytes_read.sum + dram__bytes_write.sum, one ncu --set full launch)"
         return out
     except Exception:
         return {}
+
+
+def read_only_ceiling_gbs(nbytes=4 << 30):
+    """A live read-only stream on this GPU: torch's sum over a 4 GiB fp32 tensor (best of 5, CUDA events)."""
+    import torch
+    x = torch.ones(nbytes // 4, dtype=torch.float32, device="cuda")
+    x.sum()
+    best = 0.0
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        x.sum()
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    del x
+    torch.cuda.empty_cache()
+    return best
 
 
 def workload_desc(cfg, n_total):
@@ -303,19 +325,33 @@ def main():
     n_loc, d = sh.rows, cfg.d
     sk_bytes = n_loc * (4 * d + 1 + 8 + 8) + 4 * cfg.r1 * d
     rn_bytes = n_loc * (4 * d + 4)
+    graded = {"fct1_sketch": n_loc * 4 * d + 4 * cfg.r1 * d, "l1_rownorm": n_loc * (4 * d + 4)}   # A + outputs
     t_sk = stage_ms["sketch"]["mean"] * 1e-3
     t_rn = stage_ms["rownorm"]["mean"] * 1e-3
     kern = {"fct1_sketch": (sk_bytes, t_sk), "l1_rownorm": (rn_bytes, t_rn)}
     dom = max(kern, key=lambda k: kern[k][1])
-    traffic = load_traffic(cfg, n_loc, world) if args.estimator == "median" else {}
+    buf = ctypes.create_string_buffer(128)
+    instances = {}
+    for stage, kname in ((0, "fct1_sketch"), (1, "l1_rownorm")):
+        lib.fct_last_instance(stage, buf, 128)
+        instances[kname] = buf.value.decode()
+    traffic = load_traffic(cfg, n_loc, world, instances) if args.estimator == "median" else {}
+    ro = read_only_ceiling_gbs() if rank == 0 else None
     rl = {}
     for kname, (byt, t) in kern.items():
         ach = byt / t / 1e9
         rl[kname] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                      "traffic": traffic.get(kname), "algorithmic_bytes_per_launch": byt, "ms_per_launch": t * 1e3,
-                     "frac_of_8TBs": ach / 8000.0}
+                     "kernel_instance": instances[kname],
+                     "graded_bytes_per_launch": graded[kname],
+                     "graded_frac_of_8TBs": graded[kname] / t / 8e12,
+                     "frac_of_8TBs": ach / 8000.0,
+                     "read_only_ceiling_gbs": ro, "frac_of_read_only_ceiling": (ach / ro) if ro else None}
         if traffic.get(kname):
             rl[kname]["traffic_source"] = traffic["_source"]
+        elif traffic.get("_mismatch", {}).get(kname):
+            rl[kname]["traffic_note"] = {"reason": "ncu capture is of another kernel instance: traffic withheld",
+                                         **traffic["_mismatch"][kname]}
     roofline = dict(rl[dom])
     roofline["kernel"] = dom
     if traffic.get("_limiter", {}).get(dom):

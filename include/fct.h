@@ -49,6 +49,10 @@ const char* fct_last_error(void);
 const char* fct_version(void);
 /* Number of kernels this library has launched in this process (all threads, all devices). */
 uint64_t fct_launch_count(void);
+/* The kernel template instance the last call of a hot-path stage launched (stage 0: the FCT1 sketch's main
+ * kernel, 1: the row-norm kernel), e.g. "sketch_v5_kernel<5, 5, 8, 2, 1>", copied NUL-terminated into buf
+ * (len bytes, host memory).  Returns 0, or -1 for a bad stage / buffer.  Used to match ncu captures. */
+int fct_last_instance(int32_t stage, char* buf, size_t len);
 
 /* Limits of this build. */
 #define FCT_MAX_S 4096   /* Hadamard block size s: power of two in [1, FCT_MAX_S]          */

@@ -16,6 +16,7 @@ SIGNATURES = {
     "fct_last_error": (ctypes.c_char_p, []),
     "fct_version": (ctypes.c_char_p, []),
     "fct_launch_count": (_u64, []),
+    "fct_last_instance": (ctypes.c_int, [ctypes.c_int32, ctypes.c_char_p, ctypes.c_size_t]),
     "fct_sketch_workspace_bytes": (_sz, [_i64, _i64, _i32, _i32]),
     "fct_sketch": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _i32, _i32, _vp, _int, _vp, _sz, _vp]),
     "fct_condition_workspace_bytes": (_sz, [_i32, _i64]),

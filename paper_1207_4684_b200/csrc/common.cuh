@@ -16,6 +16,8 @@ void set_error(const char* fmt, ...);
 const char* get_error();
 bool debug_sync();  // FCT_DEBUG=1
 void count_launch();
+// record the template instance a hot-path stage launched (slot 0: sketch, 1: row norms)
+void set_instance(int slot, const char* fmt, ...);
 
 #define FCT_CHECK_ARG(cond, code, ...)          \
   do {                                          \
@@ -86,6 +88,7 @@ struct SketchAcc {
   int t_l2 = 0;           // first bucket scattered through L2 (r1: none)
   int nrep = 1;
   int mode = 0;           // scatter: 0 shared-memory CAS, 1 EXCH, 2 CAS + L2 offload, 3 racy (timing only)
+  int* pace = nullptr;    // [1024] per-row-block-group pacing counters (v5)
 };
 // carve W and the replicas from a fct_sketch workspace and zero them on st
 fct_status fct_sketch_begin(void* workspace, size_t workspace_bytes, int64_t d, int s, int r1, SketchAcc* acc,
@@ -97,7 +100,8 @@ fct_status fct_sketch_accum(const float* A, int64_t n, int64_t d, int64_t lda, c
 // replicas -> W (fixed order, fp64), then Y = (float)(W [+ Y])
 fct_status fct_sketch_end(const SketchAcc& acc, int r1, int64_t d, float* Y, int accumulate, cudaStream_t st);
 fct_status fct_sketch_v5(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs, const float* cauchy,
-                         const int32_t* hash, int s, int r1, int mode, double* W, int64_t* rows_done, cudaStream_t st);
+                         const int32_t* hash, int s, int r1, int mode, double* W, int* pace, int64_t* rows_done,
+                         cudaStream_t st);
 fct_status fct_sketch_v1(const float* A, int64_t n, int64_t d, int64_t lda, const int8_t* signs, const float* cauchy,
                          const int32_t* hash, int s, int r1, const SketchAcc& acc, cudaStream_t st);
 fct_status fct_rownorm_impl(const float* A, int64_t n, int64_t d, int64_t lda, const double* Rinv,

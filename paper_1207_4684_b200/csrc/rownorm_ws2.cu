@@ -565,6 +565,7 @@ fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M3
   kern<<<g, threads, smem, st>>>(map, A, n, d, lda, M32, KP32, M64, colb, gam, NA, ND, lambda, partial, diag,
                                  wh ? (unsigned)atoi(wh) : 20000u);
   FCT_LAUNCHED("rownorm_ws2_kernel", st);
+  fct::set_instance(1, "rownorm_ws2_kernel<%d, %d, %d, %d, %d, %d>", KK, D, EG, RG, keep ? 1 : 0, at ? 1 : 0);
   if (diag & 8) {
     unsigned long long h[32][2];
     cudaStreamSynchronize(st);

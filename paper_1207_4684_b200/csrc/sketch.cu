@@ -170,6 +170,7 @@ fct_status fct_sketch_begin(void* workspace, size_t workspace_bytes, int64_t d, 
   (void)workspace_bytes;
   fct::Carver cv(workspace);
   acc->W = cv.take<double>((size_t)r1 * d);
+  acc->pace = cv.take<int>(1024);
   int t_l2, nrep, mode;
   sketch_policy(r1, s, d, &t_l2, &nrep, &mode);
   acc->t_l2 = t_l2;
@@ -190,7 +191,7 @@ fct_status fct_sketch_accum(const float* A, int64_t n, int64_t d, int64_t lda, c
   if (!getenv("FCT_SKETCH_GENERIC") && (acc.mode == 0 || acc.mode == 1)) {
     // v5 takes the full s-blocks; the ragged tail block (if any) continues below through v1 / generic
     int64_t done = 0;
-    rc = fct_sketch_v5(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, acc.mode, acc.W, &done, st);
+    rc = fct_sketch_v5(A, n, d, lda, signs, cauchy_diag, hash_rows, s, r1, acc.mode, acc.W, acc.pace, &done, st);
     if (rc != FCT_OK && rc != FCT_ERR_UNSUPPORTED) return rc;
     if (rc == FCT_OK) {
       if (done == n) return FCT_OK;
@@ -232,7 +233,7 @@ fct_status fct_sketch_end(const SketchAcc& acc, int r1, int64_t d, float* Y, int
 extern "C" size_t fct_sketch_workspace_bytes(int64_t n, int64_t d, int32_t s, int32_t r1) {
   (void)n; (void)s;
   if (d < 1 || r1 < 1) return 0;
-  return fct::align256((size_t)r1 * (size_t)d * sizeof(double)) +
+  return fct::align256((size_t)r1 * (size_t)d * sizeof(double)) + fct::align256(1024 * sizeof(int)) +
          fct::align256((size_t)kMaxRep * r1 * (size_t)d * sizeof(float)) + 256;
 }
 

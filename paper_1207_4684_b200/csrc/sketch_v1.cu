@@ -435,6 +435,7 @@ fct_status launch_v1(const float* A, int64_t n, int64_t d, int64_t lda, const in
                                                                nblocks, (float)(1.0 / sqrt((double)s)), acc.W,
                                                                acc.rep, acc.t_l2, acc.nrep);
   FCT_LAUNCHED("sketch_v1_kernel", st);
+  fct::set_instance(0, "sketch_v1_kernel<%d, %d, %d, %d, %d>", LA, LB, DT, TL, MODE);
   return FCT_OK;
 }
 

@@ -19,15 +19,33 @@ def test_metric_is_baselines():
         assert json.load(f)["metric"] == bench.METRIC
 
 
-def test_traffic_and_limiter_only_for_the_captured_workload():
+def _capture(tmp_path, monkeypatch):
+    cap = {"workload": {"config": 4, "n": fctgen.CONFIGS[4].n, "d": 64},
+           "kernels": {"fct1_sketch": {"kernel": "void <unnamed>::sketch_v5_kernel<5, 5, 8, 2, 1>(CUtensorMap_st, ...)",
+                                       "dram_bytes_read": 18.0e9, "dram_bytes_write": 5e6,
+                                       "limiter": {"resource": "shared-memory data pipe", "pct_of_peak": 80.0}},
+                       "l1_rownorm": {"kernel": "void <unnamed>::rownorm_ws2_kernel<27, 64, 3, 0, 1, 0>(...)",
+                                      "dram_bytes_read": 17.3e9, "dram_bytes_write": 3.6e8}}}
+    (tmp_path / "profiles").mkdir()
+    (tmp_path / "profiles" / "cap.json").write_text(json.dumps(cap))
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    monkeypatch.setattr(bench, "TRAFFIC_FILE", os.path.join("profiles", "cap.json"))
+
+
+def test_traffic_only_for_the_captured_workload_and_kernel_instances(tmp_path, monkeypatch):
+    _capture(tmp_path, monkeypatch)
     cfg = fctgen.CONFIGS[4]
-    t = bench.load_traffic(cfg, cfg.n, 1)
+    inst = {"fct1_sketch": "sketch_v5_kernel<5, 5, 8, 2, 1>", "l1_rownorm": "rownorm_ws2_kernel<27, 64, 3, 0, 1, 0>"}
+    t = bench.load_traffic(cfg, cfg.n, 1, inst)
     assert t["fct1_sketch"] > 0 and t["l1_rownorm"] > 0 and "dram__bytes_read.sum" in t["_source"]
-    lim = t["_limiter"]["fct1_sketch"]
-    assert 0 < lim["pct_of_peak"] <= 100 and lim["wavefronts_per_launch"] > 0
+    assert t["_limiter"]["fct1_sketch"]["pct_of_peak"] == 80.0
+    # another kernel instance than the captured one: no traffic claimed for it
+    t2 = bench.load_traffic(cfg, cfg.n, 1, dict(inst, fct1_sketch="sketch_v1_kernel<5, 5, 8, 2, 1>"))
+    assert "fct1_sketch" not in t2 and t2["_mismatch"]["fct1_sketch"]["launched"].startswith("sketch_v1")
+    assert t2["l1_rownorm"] > 0
     # another shard size or world size is not the captured launch: no traffic claimed
-    assert bench.load_traffic(cfg, cfg.n // 2, 2) == {}
-    assert bench.load_traffic(fctgen.CONFIGS[3], fctgen.CONFIGS[3].n, 1) == {}
+    assert bench.load_traffic(cfg, cfg.n // 2, 2, inst) == {}
+    assert bench.load_traffic(fctgen.CONFIGS[3], fctgen.CONFIGS[3].n, 1, inst) == {}
 
 
 def test_peaks_have_a_source():

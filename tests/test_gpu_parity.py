@@ -17,6 +17,11 @@ pytestmark = pytest.mark.gpu
 
 SK_TOL = 1e-5
 LAM_TOL = 1e-5
+# NEXT-1 (exact l1 norms on the tensor cores, reading R28): every row of the 9042-row config samples
+# meets north_star's 1e-5 relative lambda bar (measured r02: max 8.5e-6 at the cfg-4 shape, median 4e-7);
+# held at that bar.  The full-size fraction is measured in test_gpu_fullsize.py.
+EXACT_FAIL_FRAC = {1: 0.0, 2: 0.0, 3: 0.0, 4: 0.0, 5: 0.0}
+EXACT_MAX_REL = 1e-5
 
 
 @pytest.fixture(scope="module")
@@ -478,9 +483,17 @@ def test_rownorm_exact_configs(fct, c):
     assert lam[0] == 0.0
     assert (err <= 2.0 ** -14 * bnd + 2.0 ** -17 * lam_o).all(), f"max err/bound {np.max(err / np.maximum(bnd, 1e-300)):.3e}"
     np.testing.assert_allclose(float(tot.item()), lam.sum(), rtol=1e-12)
-    # how many rows also meet the pure 1e-5 relative bar (reported, not required)
-    frac = float(np.mean(err <= 1e-5 * lam_o))
-    assert frac > 0.5
+    # the pure 1e-5 relative bar (north_star's lambda bar): fp32 accumulation cannot be certified to it, so the
+    # fraction of rows above it is measured and bounded (reading R28); the worst relative error too
+    rel = err / np.maximum(lam_o, 1e-300)
+    fail = float(np.mean(rel[3:] > 1e-5))
+    import json, os
+    if os.path.isdir("gpurun_out"):
+        with open("gpurun_out/rownorm_exact_rel.jsonl", "a") as f:
+            f.write(json.dumps({"config": c, "rows": int(len(rel) - 3), "frac_over_1e-5": fail,
+                                "max_rel": float(rel[3:].max()), "median_rel": float(np.median(rel[3:]))}) + "\n")
+    assert fail <= EXACT_FAIL_FRAC[c], (fail, float(rel[3:].max()))
+    assert rel[3:].max() <= EXACT_MAX_REL
 
 
 def test_rownorm_exact_identity_and_errors(fct):
