@@ -12,7 +12,7 @@ HEADER = os.path.join(ROOT, "include", "fct.h")
 def declared_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    names = re.findall(r"^\s*(?:const\s+char\s*\*|size_t|fct_status|uint64_t)\s+(\w+)\s*\(", src, flags=re.M)
+    names = re.findall(r"^\s*(?:const\s+char\s*\*|size_t|fct_status|uint64_t|int)\s+(\w+)\s*\(", src, flags=re.M)
     return sorted(set(names))
 
 
