@@ -218,6 +218,49 @@ def cpu_model():
     return None
 
 
+# ---------------------------------------------------------------------------------------- timed region
+def run_timed(step, K, W, world, names, cuda=True, before=None, sampler=None):
+    """The contract's timed region: W untimed warm-up steps, then EXACTLY K steps bracketed by a barrier and a
+    device synchronize on both sides, timed on the device (CUDA events on the launching stream; wall clock
+    only for the CPU/gloo tests), reduced as the MAX over ranks.  step(events) runs one pass of the hot path and
+    records per-stage events when given a dict.  Returns (last StepResult, max-over-ranks ms for the K steps,
+    per-step event dicts or None)."""
+    import contextlib
+    import torch
+    import torch.distributed as dist
+    sync = torch.cuda.synchronize if cuda else (lambda: None)
+    res = None
+    for _ in range(W):
+        res = step(None)
+    sync()
+    if world > 1:
+        dist.barrier()
+    evs = [{k: torch.cuda.Event(enable_timing=True) for k in names} for _ in range(K)] if cuda else None
+    if before:
+        before()
+    sync()
+    if world > 1:
+        dist.barrier()
+    with (sampler or contextlib.nullcontext()):
+        if cuda:
+            e_beg, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e_beg.record()
+        t0 = time.perf_counter()
+        for it in range(K):
+            res = step(evs[it] if evs else None)
+        if cuda:
+            e_end.record()
+        sync()
+        t1 = time.perf_counter()
+    if world > 1:
+        dist.barrier()
+    ms = e_beg.elapsed_time(e_end) if cuda else (t1 - t0) * 1e3
+    t_local = torch.tensor([ms], dtype=torch.float64, device="cuda" if cuda else "cpu")
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    return res, float(t_local.item()), evs
+
+
 # ---------------------------------------------------------------------------------------- main arm
 def main():
     ap = argparse.ArgumentParser()
@@ -285,34 +328,15 @@ def main():
     def step(events=None):
         return run_step(ops, sh, A, sg, cc, hh, pi2, cfg.s, cfg.r1, cfg.m, cfg.seed, events=events)
 
-    for _ in range(W):
-        res = step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    info = int(res.extra[0].item()) if res.extra else 0
-    # per-stage events for every timed step (on the current stream = the launching stream)
-    evs = [{k: torch.cuda.Event(enable_timing=True) for k in names} for _ in range(K)]
-    e_beg, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = [0]
     sampler = ClockSampler(local)
-    launches0 = lib.fct_launch_count()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    with sampler:
-        e_beg.record()
-        for it in range(K):
-            res = step(evs[it])
-        e_end.record()
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    launches = lib.fct_launch_count() - launches0
-    ms = e_beg.elapsed_time(e_end)
-    t_local = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-    ms_max = float(t_local.item())
+
+    def before_timed():
+        launches0[0] = lib.fct_launch_count()
+
+    res, ms_max, evs = run_timed(step, K, W, world, names, cuda=True, before=before_timed, sampler=sampler)
+    launches = lib.fct_launch_count() - launches0[0]
+    info = int(res.extra[0].item()) if res.extra else 0
     stage_ms = {}
     for a, b in zip(names, names[1:]):
         v = [e[a].elapsed_time(e[b]) for e in evs]

@@ -141,3 +141,65 @@ def test_dist_pipeline_equals_single_process(world):
     np.testing.assert_array_equal(Z, OL.coreset_rows(inp.A, gi, gw))
     x1, f1 = OL.lad(Z)
     np.testing.assert_array_equal(xh, x1)
+
+
+def _bench_worker(rank, world, port, n, q):
+    """bench.py's own timed region (run_timed: warm-up, barrier + sync on both sides, K steps, MAX over ranks)
+    driving dist.run_step end to end on a gloo process group, with the oracle stand-in ops."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = fctgen.CONFIGS[1]
+        sh = shard_rows(n, cfg.s, rank, world)
+        inp = fctgen.make_inputs(cfg, n=sh.rows, row0=sh.row0)
+        t = torch.from_numpy
+        ops = oracle_ops()
+        calls = []
+
+        def step(events):
+            calls.append(events)
+            return run_step(ops, sh, t(inp.A), t(inp.signs), t(inp.cauchy), t(inp.hash), t(inp.pi2), cfg.s, cfg.r1,
+                            cfg.m, seed=cfg.seed)
+
+        res, ms_max, evs = bench.run_timed(step, K=2, W=3, world=world, names=[], cuda=False)
+        mine = torch.tensor([ms_max], dtype=torch.float64)
+        allv = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(allv, mine)
+        gi, gw, gc = gather_samples(res)
+        q.put((rank, len(calls), [float(v.item()) for v in allv], gi.numpy(), gw.numpy(), gc))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_timed_region_on_gloo():
+    """W + K steps per rank, every rank reports the same (maximum) time, and the samples of the timed run equal the
+    single-process oracle pipeline's (the same code path bench.py runs under torchrun with NCCL)."""
+    world, n = 2, 4 * 1024 + 37
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_bench_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    outs = [q.get(timeout=600) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ncalls, times, gi, gw, gc in outs:
+        assert ncalls == 3 + 2
+        assert len(set(times)) == 1 and times[0] > 0          # max over ranks, identical on every rank
+    # single process reference
+    cfg = fctgen.CONFIGS[1]
+    inp = fctgen.make_inputs(cfg, n=n)
+    Y, _ = oracle.sketch(inp.A, inp.signs, inp.cauchy, inp.hash, cfg.s, cfg.r1)
+    _, Rinv, _ = oracle.condition(Y)
+    lam, tot = oracle.rownorm(inp.A, Rinv, inp.pi2)
+    p = oracle.probs(lam, tot).astype(np.float32)
+    oi, ow, oc = oracle.sample(p, cfg.m, seed=cfg.seed)
+    _, _, _, gi, gw, gc = outs[0]
+    assert gc == oc
+    np.testing.assert_array_equal(gi, oi)
+    np.testing.assert_array_equal(gw, ow)
