@@ -132,8 +132,12 @@ __device__ __forceinline__ void scatter(float* __restrict__ P, const int (&addr)
   }
 }
 
-template <int LA, int LB, int DT, int TILES_>
+template <int LA, int LB, int DT, int TILES_, bool SA_ = false>
 struct Geo5 {
+  // SA (shared aux): the identity and Hadamard halves of the aux use ONE pair of buffers in turn (the Hadamard
+  // half is loaded after phase A has consumed the identity half) and the signs are read from global memory, so
+  // that two tile groups fit next to P at r1 = 8192 (the cfg-5 geometry)
+  static constexpr bool SA = SA_;
   static constexpr int S = 1 << (LA + LB);
   static constexpr int RA = 1 << LA;            // contiguous rows per thread, phase A
   static constexpr int RB = 1 << LB;            // strided rows per thread per group, phase B
@@ -149,7 +153,7 @@ struct Geo5 {
   static constexpr size_t half_bytes = (size_t)S * 4;              // one aux half (C or B) of a block
   static constexpr size_t sign_bytes = (size_t)(S + 1023) / 1024 * 1024;
   // per tile group: tile | C_id | B_id | C_had | B_had | signs (aux halves 1024-B aligned for SWIZZLE_128B)
-  static constexpr size_t group_bytes = tile_bytes + 4 * half_bytes + sign_bytes;
+  static constexpr size_t group_bytes = tile_bytes + (SA ? 2 * half_bytes : 4 * half_bytes + sign_bytes);
 };
 
 // physical row of logical row r in the exchange layout: conflict-free for both phases' access patterns
@@ -160,13 +164,13 @@ __device__ __forceinline__ int xswz(int r) {
 // word offset of aux entry e in a SWIZZLE_128B-staged array of 32-entry (128-B) rows
 __device__ __forceinline__ int aux_off(int e) { return (e & ~31) | (((((e >> 2) & 7) ^ ((e >> 5) & 7)) << 2) | (e & 3)); }
 
-template <int LA, int LB, int DT, int TL, int MODE>
-__global__ void __launch_bounds__(Geo5<LA, LB, DT, TL>::THREADS, 1)
+template <int LA, int LB, int DT, int TL, int MODE, bool SA>
+__global__ void __launch_bounds__(Geo5<LA, LB, DT, TL, SA>::THREADS, 1)
 sketch_v5_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
                  const __grid_constant__ CUtensorMap tmH, const int8_t* __restrict__ signs, int r1, int d,
                  int nslices, int64_t nblocks, float inv_sqrt_s, double* __restrict__ W, int* __restrict__ pace,
                  int pace_every) {
-  using Gm = Geo5<LA, LB, DT, TL>;
+  using Gm = Geo5<LA, LB, DT, TL, SA>;
   constexpr int S = Gm::S, RA = Gm::RA, RB = Gm::RB, NG = Gm::NG, NT = Gm::NT, NB = Gm::NB, TILES = Gm::TILES,
                 G = Gm::G;
   // SWIZZLE_128B destinations must be 1024-byte aligned: the dynamic region is declared 1024-aligned (the
@@ -184,9 +188,9 @@ sketch_v5_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   float* tile = (float*)gb;
   const float* sCi = (const float*)(gb + Gm::tile_bytes);
   const int* sHi = (const int*)(gb + Gm::tile_bytes + Gm::half_bytes);
-  const float* sCh = (const float*)(gb + Gm::tile_bytes + 2 * Gm::half_bytes);
-  const int* sHh = (const int*)(gb + Gm::tile_bytes + 3 * Gm::half_bytes);
-  const int8_t* sSg = (const int8_t*)(gb + Gm::tile_bytes + 4 * Gm::half_bytes);
+  const float* sCh = SA ? sCi : (const float*)(gb + Gm::tile_bytes + 2 * Gm::half_bytes);
+  const int* sHh = SA ? sHi : (const int*)(gb + Gm::tile_bytes + 3 * Gm::half_bytes);
+  const int8_t* sSg = (const int8_t*)(gb + Gm::tile_bytes + 4 * Gm::half_bytes);   // !SA only
   float* P = (float*)(smraw + (size_t)TILES * Gm::group_bytes);
 
   for (int e = threadIdx.x; e < r1 * DT; e += blockDim.x) P[e] = 0.f;
@@ -202,12 +206,12 @@ sketch_v5_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     mb_expect(&bar_t[tg], (unsigned)Gm::tile_bytes);
     tma4(tile, &tmA, c0, 0, 0, (int)bb, &bar_t[tg]);
   };
-  auto issue_id = [&](int64_t bb) {   // identity-half C and B, and the block's signs
-    mb_expect(&bar_i[tg], (unsigned)(2 * Gm::half_bytes + S));
+  auto issue_id = [&](int64_t bb) {   // identity-half C and B, and the block's signs (!SA)
+    mb_expect(&bar_i[tg], (unsigned)(2 * Gm::half_bytes + (SA ? 0 : S)));
     const int row = (int)((2 * bb * S + S) / 32);
     tma2((void*)sCi, &tmC, 0, row, &bar_i[tg]);
     tma2((void*)sHi, &tmH, 0, row, &bar_i[tg]);
-    bulk((void*)sSg, signs + bb * S, (unsigned)S, &bar_i[tg]);
+    if (!SA) bulk((void*)sSg, signs + bb * S, (unsigned)S, &bar_i[tg]);
   };
   auto issue_had = [&](int64_t bb) {  // Hadamard-half C and B
     mb_expect(&bar_h[tg], (unsigned)(2 * Gm::half_bytes));
@@ -221,7 +225,7 @@ sketch_v5_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (lt == 0 && b < nblocks) {
     issue_tile(b);
     issue_id(b);
-    issue_had(b);
+    if (!SA) issue_had(b);
   }
   unsigned phase = 0;
   const float sc_h = 4.f * inv_sqrt_s;
@@ -251,7 +255,7 @@ sketch_v5_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       static_assert(RA % 16 == 0, "phase A sign vectors");
 #pragma unroll
       for (int k0 = 0; k0 < RA; k0 += 16) {   // 16 signs per 16-B load
-        const int4 sv = *(const int4*)(sSg + RA * g + k0);
+        const int4 sv = SA ? __ldg((const int4*)(signs + b * S + RA * g + k0)) : *(const int4*)(sSg + RA * g + k0);
         const int sw[4] = {sv.x, sv.y, sv.z, sv.w};
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
@@ -278,7 +282,10 @@ sketch_v5_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       fwht<RA>(x);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       nbar(1 + tg, NT);   // tile and identity aux consumed
-      if (lt == 0 && bn < nblocks) issue_id(bn);
+      if (lt == 0) {
+        if (SA) issue_had(b);                 // the Hadamard half of THIS block into the same buffers
+        else if (bn < nblocks) issue_id(bn);
+      }
 #pragma unroll
       for (int k = 0; k < RA; ++k) tile[xswz<LA, G>(RA * g + k) * DT + c] = x[k];
     }
@@ -315,7 +322,10 @@ sketch_v5_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     nbar(1 + tg, NT);   // the Hadamard aux is free
-    if (lt == 0 && bn < nblocks) issue_had(bn);
+    if (lt == 0 && bn < nblocks) {
+      if (SA) issue_id(bn);
+      else issue_had(bn);
+    }
   }
   __syncthreads();
   for (int e = threadIdx.x; e < r1 * DT; e += blockDim.x) {
@@ -337,16 +347,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return fn;
 }
 
-template <int LA, int LB, int DT, int TL>
+template <int LA, int LB, int DT, int TL, bool SA = false>
 size_t v5_smem(int r1) {
-  using Gm = Geo5<LA, LB, DT, TL>;
+  using Gm = Geo5<LA, LB, DT, TL, SA>;
   return (size_t)TL * Gm::group_bytes + (size_t)r1 * DT * sizeof(float);
 }
 
-template <int LA, int LB, int DT, int TL, int MODE>
+template <int LA, int LB, int DT, int TL, int MODE, bool SA = false>
 fct_status launch_v5(const float* A, int64_t nfull, int64_t d, int64_t lda, const int8_t* signs, const float* cauchy,
                      const int32_t* hash, int s, int r1, double* W, int* pace, cudaStream_t st) {
-  using Gm = Geo5<LA, LB, DT, TL>;
+  using Gm = Geo5<LA, LB, DT, TL, SA>;
   auto enc = encoder();
   FCT_CHECK_ARG(enc, FCT_ERR_CUDA, "fct_sketch: cuTensorMapEncodeTiled unavailable");
   const int64_t nblocks = nfull / s;
@@ -373,8 +383,8 @@ fct_status launch_v5(const float* A, int64_t nfull, int64_t d, int64_t lda, cons
     if (cr != CUDA_SUCCESS) return FCT_ERR_UNSUPPORTED;
   }
   const int nslices = (int)((d + DT - 1) / DT);
-  const size_t smem = v5_smem<LA, LB, DT, TL>(r1);
-  auto kern = sketch_v5_kernel<LA, LB, DT, TL, MODE>;
+  const size_t smem = v5_smem<LA, LB, DT, TL, SA>(r1);
+  auto kern = sketch_v5_kernel<LA, LB, DT, TL, MODE, SA>;
   int pace_every = 16;   // measured: DRAM reads 34.0 -> 22.9 GB at 8 (cfg 4), time within 1 %
   if (const char* e = getenv("FCT_SKETCH_PACE")) pace_every = atoi(e);   // 0: no pacing
   if (pace_every <= 0) pace = nullptr;
@@ -392,7 +402,7 @@ fct_status launch_v5(const float* A, int64_t nfull, int64_t d, int64_t lda, cons
   kern<<<(unsigned)(ngrp * nslices), Gm::THREADS, smem, st>>>(mA, mC, mH, signs, r1, (int)d, nslices, nblocks,
                                                                (float)(1.0 / sqrt((double)s)), W, pace, pace_every);
   FCT_LAUNCHED("sketch_v5_kernel", st);
-  fct::set_instance(0, "sketch_v5_kernel<%d, %d, %d, %d, %d>", LA, LB, DT, TL, MODE);
+  fct::set_instance(0, "sketch_v5_kernel<%d, %d, %d, %d, %d, %s>", LA, LB, DT, TL, MODE, SA ? "true" : "false");
   return FCT_OK;
 }
 
@@ -416,6 +426,10 @@ fct_status fct_sketch_v5(const float* A, int64_t n, int64_t d, int64_t lda, cons
       (DT_ <= 8 || d >= DT_))                                                                                  \
     rc = mode == 0 ? launch_v5<LA_, LB_, DT_, TL_, 0>(A, nfull, d, lda, signs, cauchy, hash, s, r1, W, pace, st)      \
                    : launch_v5<LA_, LB_, DT_, TL_, 1>(A, nfull, d, lda, signs, cauchy, hash, s, r1, W, pace, st);
+  if (rc == FCT_ERR_UNSUPPORTED && s == 2048 && v5_smem<6, 5, 8, 2>(r1) > kV5Smem && v5_smem<6, 5, 4, 2>(r1) > kV5Smem &&
+      v5_smem<6, 5, 4, 2, true>(r1) <= kV5Smem && !getenv("FCT_SKETCH_NOSA"))   // cfg-5 geometry: two tile groups
+    rc = mode == 0 ? launch_v5<6, 5, 4, 2, 0, true>(A, nfull, d, lda, signs, cauchy, hash, s, r1, W, pace, st)
+                   : launch_v5<6, 5, 4, 2, 1, true>(A, nfull, d, lda, signs, cauchy, hash, s, r1, W, pace, st);
   TRY5(6, 5, 8, 2) TRY5(6, 5, 4, 2) TRY5(6, 5, 4, 1)     // s = 2048
   TRY5(5, 5, 16, 2) TRY5(5, 5, 16, 1) TRY5(5, 5, 8, 2) TRY5(5, 5, 4, 2)    // s = 1024
   TRY5(4, 4, 16, 2) TRY5(4, 4, 8, 4) TRY5(4, 4, 4, 8)                      // s = 256
