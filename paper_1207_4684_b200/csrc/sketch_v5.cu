@@ -402,7 +402,7 @@ fct_status launch_v5(const float* A, int64_t nfull, int64_t d, int64_t lda, cons
   kern<<<(unsigned)(ngrp * nslices), Gm::THREADS, smem, st>>>(mA, mC, mH, signs, r1, (int)d, nslices, nblocks,
                                                                (float)(1.0 / sqrt((double)s)), W, pace, pace_every);
   FCT_LAUNCHED("sketch_v5_kernel", st);
-  fct::set_instance(0, "sketch_v5_kernel<%d, %d, %d, %d, %d, %s>", LA, LB, DT, TL, MODE, SA ? "true" : "false");
+  fct::set_instance(0, "sketch_v5_kernel<%d, %d, %d, %d, %d, %d>", LA, LB, DT, TL, MODE, SA ? 1 : 0);   // ncu's spelling
   return FCT_OK;
 }
 

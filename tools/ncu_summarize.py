@@ -13,8 +13,9 @@ from collections import defaultdict
 
 
 def launches(path):
-    rows = [r for r in csv.reader(open(path)) if r]
-    h = rows[0]
+    rows = [r for r in csv.reader(open(path)) if r and not r[0].startswith("==")]
+    h = next(r for r in rows if "Kernel Name" in r)
+    rows = rows[rows.index(h):]
     ki, mi, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
     agg = defaultdict(list)
     for r in rows[1:]:
@@ -29,19 +30,25 @@ def launches(path):
 def full(rep, cfg, n, d):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h = rows[0]
+    h, units = rows[0], rows[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3, "msecond": 1e6,
+             "second": 1e9, "ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9, "cycle": 1, "Kcycle": 1e3, "Mcycle": 1e6}
     res = {"source": f"ncu --set full --clock-control none --import-source on, one launch per kernel ({rep})",
            "workload": {"config": int(cfg), "n": int(n), "d": int(d)}, "kernels": {}}
     for r in rows[2:]:
         if len(r) != len(h):
             continue
-        g = lambda m: float(r[h.index(m)].replace(",", "")) if m in h and r[h.index(m)] not in ("", "n/a") else None
+        def g(m):
+            if m not in h or r[h.index(m)] in ("", "n/a"):
+                return None
+            return float(r[h.index(m)].replace(",", "")) * scale.get(units[h.index(m)], 1)
         name = r[h.index("Kernel Name")]
         key = "fct1_sketch" if "sketch" in name else ("l1_rownorm" if "rownorm" in name else name)
         cyc = g("sm__cycles_elapsed.avg")
         wf = g("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")
         rec = {"kernel": name,
                "gpu_time_ms_under_ncu": g("gpu__time_duration.sum") / 1e6 if g("gpu__time_duration.sum") else None,
+               "sm_cycles_elapsed_note": "sm__cycles_elapsed.avg (per SM)",
                "dram_bytes_read": g("dram__bytes_read.sum"), "dram_bytes_write": g("dram__bytes_write.sum"),
                "smem_wavefronts": wf, "smem_bank_conflicts": g("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
                "warp_instructions": g("smsp__inst_executed.sum"), "sm_cycles_elapsed_avg": cyc,
