@@ -220,7 +220,7 @@ int64_t or_sample(const float* p, const double* u, int64_t n, int64_t row_base, 
   for (int64_t i = 0; i < n; ++i) {
     const double pi = (double)p[i];
     const double mp = (double)m * pi;
-    const double phat = mp < 1.0 ? mp : 1.0;
+    const double phat = mp < 1.0 ? mp : (mp >= 1.0 ? 1.0 : 0.0);   /* NaN p_i: never sampled (R31) */
     double ui;
     if (u) ui = u[i];
     else ui = (double)(or_rng_u64(seed, 9, (uint64_t)(row_base + i)) >> 11) * 0x1.0p-53;

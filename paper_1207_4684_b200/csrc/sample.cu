@@ -25,7 +25,7 @@ struct Decide {
   uint64_t key;      // mix64(seed + G * (9 + 1))
   __device__ __forceinline__ bool operator()(int64_t i, double& phat) const {
     const double mp = m * (double)p[i];
-    phat = mp < 1.0 ? mp : 1.0;
+    phat = mp < 1.0 ? mp : (mp >= 1.0 ? 1.0 : 0.0);   // NaN p: never sampled (R31)
     double ui;
     if (u) ui = u[i];
     else ui = (double)(mix64(key + 0x9E3779B97F4A7C15ULL * (uint64_t)(row_base + i + 1)) >> 11) * 0x1.0p-53;
@@ -34,7 +34,7 @@ struct Decide {
   // the same decision from an already-rounded p value
   __device__ __forceinline__ bool decide_p(float pi, int64_t i, double& phat) const {
     const double mp = m * (double)pi;
-    phat = mp < 1.0 ? mp : 1.0;
+    phat = mp < 1.0 ? mp : (mp >= 1.0 ? 1.0 : 0.0);
     const double ui = (double)(mix64(key + 0x9E3779B97F4A7C15ULL * (uint64_t)(row_base + i + 1)) >> 11) * 0x1.0p-53;
     return ui < phat;
   }

@@ -335,6 +335,19 @@ def test_probs_sample_fused_bit_exact(fct, n, m, row_base, cap):
     np.testing.assert_array_equal(i2.cpu().numpy()[:k], idx.cpu().numpy()[:k])
 
 
+def test_sample_nan_probabilities_are_never_sampled(fct):
+    """NaN p (e.g. after a conditioning failure) -> p_hat = 0 on both sides (R31); bit-exact."""
+    p = np.abs(np.random.default_rng(8).standard_cauchy(5000)).astype(np.float32) * 1e-4
+    p[::3] = np.nan
+    p[7] = np.inf
+    oi, ow, oc = oracle.sample(p, 300, seed=4)
+    idx, w, cnt = fct.l1_sample(dev(p), 300, seed=4)
+    gi, gw, gc = fct.trim(idx, w, cnt)
+    assert gc == oc and not np.isnan(p[oi]).any()
+    np.testing.assert_array_equal(gi.numpy(), oi)
+    np.testing.assert_array_equal(gw.numpy(), ow)
+
+
 # ---------------------------------------------------------------- whole pipeline vs oracle pipeline
 @pytest.mark.parametrize("c", [1, 2])
 def test_pipeline_end_to_end(fct, c):

@@ -130,6 +130,12 @@ def test_sample_extremes_and_weights():
     # weights are 1/phat with phat = min(1, m p) in fp64 from the fp32 p
     for i, wi in zip(idx, w):
         assert wi == 1.0 / min(1.0, 5 * float(p[i]))
+    # an undefined probability (NaN) is never sampled, even with explicit uniforms of 0 (R31); +inf is
+    # p_hat = 1
+    p2 = np.full(64, np.nan, np.float32)
+    p2[5] = np.inf
+    idx2, w2, cnt2 = oracle.sample(p2, m=5, seed=3, u=np.zeros(64))
+    assert cnt2 == 1 and idx2.tolist() == [5] and w2.tolist() == [1.0]
 
 
 def test_sample_explicit_uniforms_rule():
