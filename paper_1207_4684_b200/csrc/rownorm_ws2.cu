@@ -174,13 +174,20 @@ struct Smem {   // byte offsets inside the 1024-aligned dynamic shared memory
   int a, b, m64, cm, nrm, cq, bars, total;
 };
 constexpr int kCQ = 4;   // candidate-descriptor ring (selection -> recompute warps)
-// fp64 M for the exact candidate recompute: read through L1 from global memory (14 KB at d = 64, k = 27)
-// so that the shared memory holds one more 32 KB tile buffer (tiles stay until their rows are final)
-constexpr bool kM64Smem = true;
+// fp64 M for the exact candidate recompute: in shared memory by default; FCT_ROWNORM_M64G=1 reads it through L1
+// from global memory instead (14 KB at d = 64, k = 27), so that the shared memory holds one more tile buffer
 
 // FCT_ROWNORM_DIAG bit 3 (diagnostics only): per-warp cycles spent in mbarrier waits and in total, CTA 0
 __device__ unsigned long long g_rn_prof[32][2];
-__device__ unsigned long long g_rn_cta[1024][2];   // per-CTA globaltimer at start / end (FCT_ROWNORM_PROF)
+__device__ unsigned long long g_rn_cta[1024][2];
+// FCT_ROWNORM_DIAG bit 4 (diagnostics only): CTA-0 timeline of the first kTrace tiles, clock64 per event:
+// 0 TMA issued, 1 split start, 2 split done, 3 MMA start, 4 MMA committed, 5 epilogue start (max over warps),
+// 6 epilogue done (max over warps), 7 selection done (max over warps)
+constexpr int kTrace = 256;
+__device__ unsigned long long g_rn_trace[kTrace][8];
+__device__ __forceinline__ void trace(bool on, int i, int ev) {
+  if (on && blockIdx.x == 0 && i < kTrace && (threadIdx.x & 31) == 0) atomicMax(&g_rn_trace[i][ev], (unsigned long long)clock64());
+}   // per-CTA globaltimer at start / end (FCT_ROWNORM_PROF)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -204,13 +211,13 @@ struct WaitClock {
     }
   }
 };
-__host__ __device__ inline Smem layout(int d, int KK, int NA, int ND, bool cq = true) {
+__host__ __device__ inline Smem layout(int d, int KK, int NA, int ND, bool cq, bool m64s) {
   const int nch = (d + 31) / 32;
   Smem s;
   s.a = 0;
   s.b = s.a + NA * nch * 16384;          // B = [M_hi | M_lo]^T: nch chunks x 64 rows x 128 B
   s.m64 = s.b + nch * 8192;
-  s.cm = s.m64 + (kM64Smem ? ((d * KK * 8 + 15) & ~15) : 0);
+  s.cm = s.m64 + (m64s ? ((d * KK * 8 + 15) & ~15) : 0);
   s.nrm = s.cm + 32 * 4;
   s.cq = s.nrm + ND * 128 * 4;           // [kCQ][128] descriptors + [kCQ][128] settled lambdas
   s.bars = s.cq + (cq ? kCQ * 128 * 8 : 0);
@@ -227,16 +234,16 @@ __global__ void __launch_bounds__(32 * (kEpiWarp0 + 4 * EG + 4 * RG), 1)
 rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ A, int64_t n, int d, int64_t lda,
                    const float* __restrict__ M32g, int KP32, const double* __restrict__ M64g,
                    const float* __restrict__ colbg, float gam, int NA, int ND, float* __restrict__ lambda,
-                   double* __restrict__ partial, int diag, unsigned whint) {
+                   double* __restrict__ partial, int diag, unsigned whint, int m64s) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* base = smraw + ((1024u - (tcx::su32(smraw) & 1023u)) & 1023u);
   const int dd = D ? D : d;
   const int nch = (dd + 31) >> 5, KP = nch * 32;
   const int tile_floats = nch * 128 * 32;
-  const Smem L = layout(dd, KK, NA, ND, RG > 0);
+  const Smem L = layout(dd, KK, NA, ND, RG > 0, m64s != 0);
   float* sA = (float*)(base + L.a);
   float* sB = (float*)(base + L.b);
-  const double* M64 = kM64Smem ? (const double*)(base + L.m64) : M64g;
+  const double* M64 = m64s ? (const double*)(base + L.m64) : M64g;
   float* cm = (float*)(base + L.cm);
   float* norms = (float*)(base + L.nrm);
   uint64_t* tma_full = (uint64_t*)(base + L.bars);   // [NA]  tile landed
@@ -287,7 +294,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
     const float hi = tcx::trunc_tf32(m);
     sB[(l >> 5) * 64 * 32 + jj * 32 + ((((l & 31) >> 2) ^ (jj & 7)) << 2) + (l & 3)] = jj < 32 ? hi : m - hi;
   }
-  if (kM64Smem)
+  if (m64s)
     for (int e = tid; e < KK * dd; e += blockDim.x) ((double*)(base + L.m64))[e] = M64g[e];
   for (int e = tid; e < 32; e += blockDim.x) cm[e] = e < KK ? colbg[2 * e] : 0.f;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -298,6 +305,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
   const int acols = abuf_cols<AT>(KP);
   const uint32_t dcol0 = 2u * acols;   // TMEM: [A buf 0][A buf 1][D 0] ... [D ND-1], D = 64 columns
   const bool prof = (diag & 8) != 0;
+  const bool trc = (diag & 16) != 0;
   diag &= 7;
   WaitClock wc(prof);
   if (prof && threadIdx.x == 0) g_rn_cta[blockIdx.x][0] = gtimer();
@@ -315,6 +323,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
       const int sl = i & 1;
       wc.wait([&] { tcx::bar_wait(&tma_full[sa], pa); });
       if (i >= 2) wc.wait([&] { tcx::bar_wait(&at_free[sl], (unsigned)(((i - 2) >> 1) & 1)); });
+      trace(trc, i, 1);
       const float* tile = sA + sa * tile_floats;
       const uint32_t tb = tm + lane_off + (uint32_t)(sl * acols);
       float s2 = 0.f, s2b = 0.f;
@@ -346,6 +355,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) tcx::bar_arrive(&at_full[sl]);
+      trace(trc, i, 2);
       if (i >= ND) wc.wait([&] { tcx::bar_wait(&d_free[sd], pd ^ 1u); });
       norms[sd * 128 + tid] = s2 + s2b;
       __syncwarp();
@@ -360,6 +370,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
       unsigned pa = 0;
       for (int j = 0; j < my_tiles; ++j) {
         if (j >= NA) wc.wait([&] { tcx::bar_wait(&a_free[sa], pa ^ 1u); });
+        trace(trc, j, 0);
         tcx::tma_tile(sA + sa * tile_floats, &tmA, nch, (t0 + j * tstep) * 128, &tma_full[sa]);
         if (++sa == NA) { sa = 0; pa ^= 1u; }
       }
@@ -378,6 +389,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
         wc.wait([&] { tcx::bar_wait(&at_full[sl], (unsigned)((i >> 1) & 1)); });   // implies the TMA tile has landed
         if (i >= ND) wc.wait([&] { tcx::bar_wait(&d_free[sd], pd ^ 1u); });
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        trace(trc, i, 3);
         const uint32_t tD = tm + dcol0 + (uint32_t)(sd * 64);
         const uint32_t tA = tm + (uint32_t)(sl * acols);
         const uint64_t a0 = a00 + (uint64_t)((sa * tile_floats * 4) >> 4);
@@ -400,6 +412,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
         tcx::mma_commit(&d_full[sd]);
         tcx::mma_commit(&at_free[sl]);
         if (!KEEP) tcx::mma_commit(&a_free[sa]);
+        trace(trc, i, 4);
         if (++sa == NA) sa = 0;
         if (++sd == ND) { sd = 0; pd ^= 1u; }
       }
@@ -419,6 +432,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
         tcx::bar_wait_sleep(&n_full[sd], ph, whint);
       });
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      trace(trc, i, 5);
       uint32_t dv[32];
       {
         uint32_t dw[32];
@@ -440,16 +454,16 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
         if (diag >= 2) lam = __uint_as_float(dv[0]) + n2;   // diag (profiling only): no epilogue arithmetic
         else fin = certify<KK, D, KEEP>(dv, n2, cm, gam, tile, A + row * lda, r, dd, M64, lam, desc);
       }
+      trace(trc, i, 7);
       if (RG == 0) {
         if (row < n) {
           if (!fin) lam = diag == 1 ? 0.f : resolve<KK, D, KEEP>(desc, tile, A + row * lda, r, dd, M64);
           lambda[row] = lam;
           local += (double)lam;
         }
-        if (KEEP) {
-          __syncwarp();
-          if (lane == 0) tcx::bar_arrive(&a_free[sa]);
-        }
+        __syncwarp();
+        trace(trc, i, 6);
+        if (KEEP && lane == 0) tcx::bar_arrive(&a_free[sa]);
       } else {
         if (i >= kCQ) tcx::bar_wait(&c_free[cs], pc ^ 1u);
         cdesc[cs * 128 + r] = fin ? 0x80000000u : desc;
@@ -541,14 +555,15 @@ fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M3
   // from TMEM (TS form) when it fits next to EG + 1 accumulators.
   const bool at = 4 * KP + 64 * (EG + 1) <= 512 && getenv("FCT_ROWNORM_ATS");
   const int ND = std::min(8, (512 - 2 * (at ? 2 * KP : KP)) / 64);
+  const bool m64s = !getenv("FCT_ROWNORM_M64G");
   int NA = 0;
   for (int na = 8; na >= 2; --na)
-    if (layout(d, KK, na, ND, RG > 0).total + 1024 <= (int)kSmemMax - 2048) { NA = na; break; }
+    if (layout(d, KK, na, ND, RG > 0, m64s).total + 1024 <= (int)kSmemMax - 2048) { NA = na; break; }
   if (NA < 2 || ND < EG + 1) return FCT_ERR_UNSUPPORTED;
   // keep the tile until the epilogue is done (exact recompute from shared memory) when enough buffers fit
   const bool keep = NA >= EG + 2 && !getenv("FCT_ROWNORM_NOKEEP");
   if (RG > 0 && !keep) return FCT_ERR_UNSUPPORTED;
-  const size_t smem = (size_t)layout(d, KK, NA, ND, RG > 0).total + 1024;
+  const size_t smem = (size_t)layout(d, KK, NA, ND, RG > 0, m64s).total + 1024;
   const int g = std::max(1, std::min(grid, fct::num_sms()));
   const int threads = 32 * (kEpiWarp0 + 4 * EG + 4 * RG);
   const float gam = 6.103515625e-05f * 1.05f;   // 3xTF32 bound, 2^-14 (measured 1.9e-6) x 1.05 for roundings
@@ -556,16 +571,49 @@ fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M3
                    : (at ? rownorm_ws2_kernel<KK, D, EG, RG, false, true> : rownorm_ws2_kernel<KK, D, EG, RG, false, false>);
   FCT_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (fct::debug_sync())
-    fprintf(stderr, "[fct] rownorm_ws2<k=%d,D=%d,EG=%d,RG=%d,keep=%d,at=%d>: grid %d NA %d ND %d smem %zu\n", KK, D, EG,
-            RG, (int)keep, (int)at, g, NA, ND, smem);
+    fprintf(stderr, "[fct] rownorm_ws2<k=%d,D=%d,EG=%d,RG=%d,keep=%d,at=%d>: grid %d NA %d ND %d m64s %d smem %zu\n", KK, D,
+            EG, RG, (int)keep, (int)at, g, NA, ND, (int)m64s, smem);
   FCT_CUDA_RET(cudaMemsetAsync(partial, 0, sizeof(double) * grid, st));
   const char* dg = getenv("FCT_ROWNORM_DIAG");
   const int diag = dg ? atoi(dg) : 0;
+  if (diag & 16) {
+    void* tp = nullptr;
+    if (cudaGetSymbolAddress(&tp, g_rn_trace) == cudaSuccess) cudaMemsetAsync(tp, 0, sizeof(unsigned long long) * kTrace * 8, st);
+  }
   const char* wh = getenv("FCT_WAIT_HINT");
   kern<<<g, threads, smem, st>>>(map, A, n, d, lda, M32, KP32, M64, colb, gam, NA, ND, lambda, partial, diag,
-                                 wh ? (unsigned)atoi(wh) : 20000u);
+                                 wh ? (unsigned)atoi(wh) : 20000u, m64s ? 1 : 0);
   FCT_LAUNCHED("rownorm_ws2_kernel", st);
   fct::set_instance(1, "rownorm_ws2_kernel<%d, %d, %d, %d, %d, %d>", KK, D, EG, RG, keep ? 1 : 0, at ? 1 : 0);
+  if (diag & 16) {
+    static unsigned long long tr[kTrace][8];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(tr, g_rn_trace, sizeof(tr));
+    const unsigned long long z = tr[0][0];
+    fprintf(stderr, "[fct trace] tile: tma split0 split1 mma0 mma1 epi0 epi1 (cycles from tile 0's TMA issue)\n");
+    for (int i = 0; i < 64; ++i) {
+      fprintf(stderr, "[fct trace] %3d:", i);
+      for (int e = 0; e < 7; ++e) fprintf(stderr, " %8lld", tr[i][e] ? (long long)(tr[i][e] - z) : -1LL);
+      fprintf(stderr, "\n");
+    }
+    for (int e = 0; e < 7; ++e) {
+      if (!tr[200][e] || !tr[100][e]) continue;
+      fprintf(stderr, "[fct trace] event %d period %.0f cycles/tile\n", e, (double)(tr[200][e] - tr[100][e]) / 100.0);
+    }
+    const char* nm[6] = {"tma->split0", "split0->split1", "split1->mma0", "mma0->mma1", "mma1->epi0", "epi0->epi1"};
+    for (int e = 0; e < 6; ++e) {
+      double acc = 0;
+      int cnt = 0;
+      for (int i = 100; i < 200; ++i)
+        if (tr[i][e] && tr[i][e + 1]) { acc += (double)(long long)(tr[i][e + 1] - tr[i][e]); ++cnt; }
+      fprintf(stderr, "[fct trace] %-15s mean %.0f cycles\n", nm[e], cnt ? acc / cnt : -1.0);
+    }
+    double a5 = 0, a7 = 0;
+    int c5 = 0;
+    for (int i = 100; i < 200; ++i)
+      if (tr[i][5] && tr[i][7] && tr[i][6]) { a5 += (double)(long long)(tr[i][7] - tr[i][5]); a7 += (double)(long long)(tr[i][6] - tr[i][7]); ++c5; }
+    if (c5) fprintf(stderr, "[fct trace] epi0->select   mean %.0f cycles, select->epi1 mean %.0f cycles\n", a5 / c5, a7 / c5);
+  }
   if (diag & 8) {
     unsigned long long h[32][2];
     cudaStreamSynchronize(st);
