@@ -16,8 +16,8 @@
 //   1 [all CTAs]  partial Gram of the CTA's contiguous rows of X_k: rows staged in shared memory (fp64),
 //                 X_k = Y R_cum^-1 formed there with 4x4 register tiles, Gram accumulated in 4x4 register tiles;
 //   2 [all CTAs]  fixed-order reduction of the per-CTA records (8 warps x c-slices, then a fixed combine);
-//   3 [CTA 0]     blocked Cholesky (8-row panels: one warp factors the panel, all warps apply the rank-8
-//                 trailing update, 2 barriers per panel) and blocked triangular inverse (same shape);
+//   3 [CTA 0]     right-looking Cholesky and triangular inverse on the register-resident triangle (16 x 16
+//                 cyclic thread grid, one published row and one barrier per step);
 //   4 [all CTAs]  R_cum <- R_k R_cum, R_cum^-1 <- R_cum^-1 R_k^-1 (packed triangular products).
 // Deterministic: every sum has a fixed order.
 #include <cooperative_groups.h>
@@ -31,7 +31,7 @@ namespace {
 constexpr int NT = 256;        // threads per CTA (8 warps)
 constexpr int NW = NT / 32;
 constexpr int ROWS = 32;       // rows of Y staged per sub-chunk
-constexpr int NB = 8;          // Cholesky / inverse panel height
+constexpr int NBLK_MAX = FCT_MAX_D / 16;   // register blocks per thread and dimension in the factorisation
 constexpr int MAXB = FCT_MAX_D / 4;                             // 4-wide column blocks
 constexpr int MAXTILE = (MAXB * (MAXB + 1) / 2 + NT - 1) / NT;  // Gram tiles per thread
 
@@ -48,6 +48,7 @@ struct Args {
   double* Rinv;            // [d][d] output
   int* info;
   int* state;              // [1]: 0 ok, 1 restart with shift, 2 failed
+  int series;              // near-identity Grams of passes >= 1 by the second-order series (R32)
   double* Rk;              // [T] packed R_k of the current pass
   double* Rki;             // [T] packed R_k^-1
   double* C[2];            // ping-pong [T] packed cumulative R
@@ -70,6 +71,8 @@ __device__ __forceinline__ int tri_row(int e, int n) {
   return i;
 }
 
+// NBLK = ceil(d / 16) rounded up to a power of two: the factorisation's register blocks per thread and dimension
+template <int NBLK>
 __global__ void __launch_bounds__(NT, 1) cond_kernel(Args a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sm[];
@@ -87,7 +90,7 @@ __global__ void __launch_bounds__(NT, 1) cond_kernel(Args a) {
   int shifted = 0, npass = 2, nts = 0;
   const double* Rci = nullptr;   // packed cumulative R^-1 used to form X_k; nullptr on pass 0
   auto stamp = [&]() {
-    if (a.ts && blockIdx.x == 0 && tid == 0 && nts < 64) a.ts[nts++] = gtimer();
+    if (a.ts && blockIdx.x == 0 && tid == 0 && nts < 56) a.ts[nts++] = gtimer();
   };
   stamp();
   for (int pass = 0; pass < npass; ++pass) {
@@ -196,118 +199,197 @@ __global__ void __launch_bounds__(NT, 1) cond_kernel(Args a) {
     }
     grid.sync();
     stamp();
-    // ================= phase 3 (CTA 0): blocked Cholesky and blocked triangular inverse
-    if (blockIdx.x == 0) {
-      double* Gs = sm;        // packed [T]: G, then R_k (rows scaled)
-      double* Xs = sm + T;    // packed [T]: R_k^-1
-      __shared__ int fail;
-      __shared__ double sigma;
-      __shared__ double dinv[FCT_MAX_D];   // 1 / R_k[i][i]
-      if (tid == 0) { fail = 0; sigma = 0.0; }
-      for (int e = tid; e < a.nb * a.nb * 16; e += NT) {   // unpack the tile record into the packed upper triangle
+    // ================= phase 3' (passes >= 1, all CTAs): a Gram within 2^-26 of I entrywise -- the common case,
+    // X_k is already orthonormal to ~u cond(Y) -- is factored by its series instead of d serial steps
+    // (R32).  G = I + E, F1 = up(E) (strict upper part, half the diagonal), U = up(F1^T F1):
+    //   R_k = I + F1 - U,   R_k^-1 = I - F1 + U + F1^2   (dropped terms O(d^2 max|E|^3) <= 2^-64).
+    // Every CTA checks the same reduced Gram, so all take the same branch.
+    bool near = false;
+    if (pass >= 1 && a.series) {
+      int far = 0;
+      for (int e = tid; e < a.nb * a.nb * 16; e += NT) {
         const int bij = e >> 4, x = (e >> 2) & 3, y = e & 3;
         const int bi = bij / a.nb, bj = bij - bi * a.nb;
-        const int i = 4 * bi + x, j = 4 * bj + y;
-        if (bj >= bi && i < d && j < d && j >= i) Gs[pk(i, j, d)] = a.G[16 * pk(bi, bj, a.nb) + (e & 15)];
+        const int i = 4 * bi + x, c = 4 * bj + y;
+        if (bj >= bi && i <= c && c < d && !(fabs(a.G[16 * pk(bi, bj, a.nb) + (e & 15)] - (i == c ? 1.0 : 0.0)) <= 0x1p-26))
+          far = 1;
       }
+      near = !__syncthreads_or(far);
+    }
+    if (near) {
+      const int nbk = a.nb;
+      auto F1 = [&](int i, int c) -> double {   // i <= c
+        const double v = a.G[16 * pk(i >> 2, c >> 2, nbk) + 4 * (i & 3) + (c & 3)];
+        return i == c ? 0.5 * (v - 1.0) : v;
+      };
+      for (int e = blockIdx.x * NT + tid; e < T; e += gridDim.x * NT) {
+        const int i = tri_row(e, d), c = i + (e - pk(i, i, d));
+        double u0 = 0.0, u1 = 0.0, q0 = 0.0, q1 = 0.0;
+        int l = 0;
+        for (; l + 1 <= i; l += 2) {   // U[i][c] = sum_{l <= i} F1[l][i] F1[l][c]
+          u0 = fma(F1(l, i), F1(l, c), u0);
+          u1 = fma(F1(l + 1, i), F1(l + 1, c), u1);
+        }
+        if (l <= i) u0 = fma(F1(l, i), F1(l, c), u0);
+        for (l = i; l + 1 <= c; l += 2) {   // (F1^2)[i][c] = sum_{i <= l <= c} F1[i][l] F1[l][c]
+          q0 = fma(F1(i, l), F1(l, c), q0);
+          q1 = fma(F1(i, l + 1), F1(l + 1, c), q1);
+        }
+        if (l <= c) q0 = fma(F1(i, l), F1(l, c), q0);
+        const double f1 = F1(i, c), uu = (i == c ? 0.5 : 1.0) * (u0 + u1), id = i == c ? 1.0 : 0.0;
+        a.Rk[e] = id + f1 - uu;
+        a.Rki[e] = id - f1 + uu + (q0 + q1);
+      }
+    }
+    // ================= phase 3 (CTA 0): register-resident Cholesky and triangular inverse
+    // The d x d upper triangle lives in the registers of the CTA's 256 threads on a 16 x 16 cyclic grid:
+    // thread (ti, tc) = (tid / 16, tid % 16) owns the entries (ti + 16 a, tc + 16 b), a, b < nblk.  Each step of
+    // the right-looking factorisation (and of the inverse) publishes one row through shared memory and costs one
+    // barrier: d steps of ~nblk^2 FMAs per thread instead of a serial panel chain (round 2: 59 -> ~10 us / pass).
+    if (!near && blockIdx.x == 0) {
+      double* Rs = sm;            // packed [T]: R_k
+      double* buf = sm + 2 * T;   // [2][DPAD]: the published row of the current step (double-buffered)
+      const int DPAD = 16 * NBLK;
+      __shared__ int fail;
+      __shared__ double sigma;
+      const int ti = tid >> 4, tc = tid & 15;
+      constexpr int nblk = NBLK;
+      double g[NBLK][NBLK];
+      // own entries of G from the tile record (entry (i, c), i <= c: tile (i / 4, c / 4), element 4 (i % 4) + c % 4)
+#pragma unroll
+      for (int x = 0; x < NBLK; ++x)
+#pragma unroll
+        for (int y = 0; y < NBLK; ++y) {
+          const int i = ti + 16 * x, c = tc + 16 * y;
+          g[x][y] = (x < nblk && y < nblk && i <= c && c < d)
+                        ? a.G[16 * pk(i >> 2, c >> 2, a.nb) + 4 * (i & 3) + (c & 3)] : 0.0;
+        }
+      if (tid == 0) { fail = 0; sigma = 0.0; }
       __syncthreads();
-      if (pass == 0 && shifted) {   // sigma = 11 (r1 d + d (d + 1)) u ||Y||_F^2, ||Y||_F^2 = trace(G)
+      if (pass == 0 && shifted) {   // sigma = 11 (r1 d + d (d + 1)) u ||Y||_F^2, ||Y||_F^2 = trace(G) (fixed order)
+#pragma unroll
+        for (int x = 0; x < NBLK; ++x)
+          if (x < nblk && ti == tc && ti + 16 * x < d) buf[ti + 16 * x] = g[x][x];
+        __syncthreads();
         if (tid == 0) {
           double tr = 0.0;
-          for (int i = 0; i < d; ++i) tr += Gs[pk(i, i, d)];
+          for (int i = 0; i < d; ++i) tr += buf[i];
           sigma = 11.0 * ((double)a.r1 * d + (double)d * (d + 1)) * u * tr;
         }
         __syncthreads();
-        for (int i = tid; i < d; i += NT) Gs[pk(i, i, d)] += sigma;
-        __syncthreads();
+#pragma unroll
+        for (int x = 0; x < NBLK; ++x)
+          if (x < nblk && ti == tc) g[x][x] += sigma;
       }
       if (pass == 1 && !shifted) {  // CholeskyQR2's second Gram must be close to I
-        for (int i = warp; i < d; i += NW) {
-          const double* rowi = Gs + pk(i, i, d) - i;
-          for (int c = i + lane; c < d; c += 32)
-            if (!(fabs(rowi[c] - (c == i ? 1.0 : 0.0)) <= 0.5)) fail = 1;
-        }
+        int bad = 0;
+#pragma unroll
+        for (int x = 0; x < NBLK; ++x)
+#pragma unroll
+          for (int y = 0; y < NBLK; ++y) {
+            const int i = ti + 16 * x, c = tc + 16 * y;
+            if (x < nblk && y < nblk && i <= c && c < d && !(fabs(g[x][y] - (i == c ? 1.0 : 0.0)) <= 0.5)) bad = 1;
+          }
+        if (__syncthreads_or(bad) && tid == 0) fail = 1;
         __syncthreads();
       }
       stamp();
-      // ---- blocked right-looking Cholesky, G = R^T R on the packed upper triangle (row i: rowi[c], c >= i)
-      for (int jb = 0; jb < d && !fail; jb += NB) {
-        const int jn = min(NB, d - jb);
-        if (warp == 0) {   // panel rows jb .. jb+jn-1 in registers (lane: columns lane + 32k), factored by one warp
-          double v[NB][4];
+      // ---- right-looking Cholesky G = R^T R without a division or square root on the step chain: the trailing
+      // matrix is kept as H = C_j S^(j) (S^(j) the Schur complement, C_j = prod_{k<j} m_k, m_k = H[k][k] 2^-e_k in
+      // [1, 2) with 2^e_k the binade of H[k][k], both exact bit operations).  Step j publishes row j of H and every
+      // owner of (i, c), i > j, forms H[i][c] <- m_j H[i][c] - (H[j][i] 2^-e_j) H[j][c]  (= m_j (S - S_ji S_jc / s_j)
+      // scaled by C_j).  Afterwards R[j][c] = H[j][c] / sqrt(C_j H[j][j]).  A pivot that is not a positive normal
+      // number (< 2^-1000 included) fails -> shifted CholeskyQR3.
+      __shared__ double mv[FCT_MAX_D], pv[FCT_MAX_D];
+      int jf = fail ? 0 : d;   // steps done
+      if (!fail)
+        for (int j = 0; j < d; ++j) {
+          double* bj = buf + (j & 1) * DPAD;
+          const int xj = j >> 4;
+          if constexpr (NBLK >= 8) {   // publish row j (the row's owners select block row xj; measured faster at 8)
+            if (ti == (j & 15)) {
 #pragma unroll
-          for (int q = 0; q < NB; ++q)
+              for (int x = 0; x < NBLK; ++x)
+                if (x == xj)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int c = lane + 32 * k, i = jb + q;
-              v[q][k] = (q < jn && c >= i && c < d) ? Gs[pk(i, c, d)] : 0.0;
-            }
-#pragma unroll
-          for (int p = 0; p < NB; ++p) {
-            if (p < jn) {
-              const int j = jb + p, kj = j >> 5;
-              const double vj = kj == 0 ? v[p][0] : kj == 1 ? v[p][1] : kj == 2 ? v[p][2] : v[p][3];
-              const double piv = __shfl_sync(0xffffffffu, vj, j & 31);
-              if (!(piv > 0.0) || !isfinite(piv)) {
-                if (lane == 0 && !fail) fail = j + 1;
-              } else {
-                const double rs = rsqrt(piv);   // R row j = G row j / sqrt(piv); rows below: G_q -= R_j[q] R_j
-#pragma unroll
-                for (int k = 0; k < 4; ++k) v[p][k] *= rs;
-                if (lane == 0) dinv[j] = rs;
-#pragma unroll
-                for (int q = p + 1; q < NB; ++q) {
-                  if (q < jn) {
-                    const int i = jb + q, ki = i >> 5;
-                    const double wi = ki == 0 ? v[p][0] : ki == 1 ? v[p][1] : ki == 2 ? v[p][2] : v[p][3];
-                    const double f = __shfl_sync(0xffffffffu, wi, i & 31);
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) v[q][k] = fma(-f, v[p][k], v[q][k]);
+                  for (int y = 0; y < NBLK; ++y) {
+                    const int c = tc + 16 * y;
+                    if (c >= j && c < d) bj[c] = g[x][y];
                   }
-                }
-              }
+            }
+          } else {   // publish row j: block row xj selected branch-free (compile-time register indices)
+            double pr[NBLK];
+#pragma unroll
+            for (int y = 0; y < NBLK; ++y) pr[y] = g[0][y];
+#pragma unroll
+            for (int x = 1; x < NBLK; ++x)
+#pragma unroll
+              for (int y = 0; y < NBLK; ++y) pr[y] = x == xj ? g[x][y] : pr[y];
+            const bool pub = ti == (j & 15);
+#pragma unroll
+            for (int y = 0; y < NBLK; ++y) {
+              const int c = tc + 16 * y;
+              if (pub && c >= j && c < d) bj[c] = pr[y];
             }
           }
+          __syncthreads();
+          const double piv = bj[j];
+          if (!(piv >= 0x1p-1000) || !(piv <= 0x1p+1000)) {
+            jf = j;
+            break;
+          }
+          const long long pb = __double_as_longlong(piv);
+          const double m = __longlong_as_double((pb & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);   // [1, 2)
+          const double sc = __longlong_as_double((long long)(2046 - ((pb >> 52) & 0x7FF)) << 52);     // 2^-e
+          if (tid == 0) { mv[j] = m; pv[j] = piv; }
+          // every entry takes the update; outside the trailing triangle the factor is 0 and the multiplier 1, so
+          // finished rows are unchanged and entries below the diagonal collect garbage that is never read
+          double fc[NBLK];
 #pragma unroll
-          for (int q = 0; q < NB; ++q)
+          for (int y = 0; y < NBLK; ++y) {
+            const int c = tc + 16 * y;
+            const double v = bj[min(c, d - 1)];
+            fc[y] = (c > j && c < d) ? v : 0.0;
+          }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int c = lane + 32 * k, i = jb + q;
-              if (q < jn && c >= i && c < d) Gs[pk(i, c, d)] = v[q][k];
-            }
-        }
-        __syncthreads();
-        if (fail) break;
-        // trailing rank-jn update of rows i >= jb + jn: G[i][c] -= sum_q R[jb+q][i] R[jb+q][c]
-        const int i0 = jb + jn;
-        if (i0 < d) {
-          double P[NB][4];
+          for (int x = 0; x < NBLK; ++x) {
+            const int i = ti + 16 * x;
+            const bool live = i > j && i < d;
+            const double v = bj[min(i, d - 1)];
+            const double fi = live ? v * sc : 0.0, mu = live ? m : 1.0;
 #pragma unroll
-          for (int q = 0; q < NB; ++q)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int c = lane + 32 * k, j = jb + q;
-              P[q][k] = (q < jn && c >= i0 && c < d) ? Gs[pk(j, c, d)] : 0.0;
-            }
-          for (int i = i0 + warp; i < d; i += NW) {
-            double f[NB];
-#pragma unroll
-            for (int q = 0; q < NB; ++q) f[q] = q < jn ? Gs[pk(jb + q, i, d)] : 0.0;
-            double* rowi = Gs + pk(i, i, d) - i;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int c = lane + 32 * k;
-              if (c >= i && c < d) {
-                double v = rowi[c];
-#pragma unroll
-                for (int q = 0; q < NB; ++q) v = fma(-f[q], P[q][k], v);
-                rowi[c] = v;
-              }
-            }
+            for (int y = 0; y < NBLK; ++y) g[x][y] = fma(-fi, fc[y], g[x][y] * mu);
           }
         }
+      __syncthreads();
+      // rinv_i = 1 / sqrt(C_i H_ii): C by a fixed-order scan of the m_k, then R[i][c] = H[i][c] rinv_i and
+      // 1 / R[i][i] = C_i rinv_i
+      double* cs = buf + 2 * DPAD;   // [DPAD] C_i, then 1 / R[i][i]
+      double* ri = buf;              // [DPAD] rinv_i (the publication buffers are free now)
+      if (jf == d && !fail) {
+        if (tid < d) cs[tid] = tid == 0 ? 1.0 : mv[tid - 1];
         __syncthreads();
+        for (int off = 1; off < d; off <<= 1) {   // inclusive product scan (Hillis-Steele)
+          const double v = (tid < d && tid >= off) ? cs[tid - off] : 1.0;
+          __syncthreads();
+          if (tid < d) cs[tid] *= v;
+          __syncthreads();
+        }
+        if (tid < d) {
+          const double r = rsqrt(cs[tid] * pv[tid]);
+          ri[tid] = r;
+          cs[tid] = cs[tid] * r;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int x = 0; x < NBLK; ++x)
+#pragma unroll
+          for (int y = 0; y < NBLK; ++y) {
+            const int i = ti + 16 * x, c = tc + 16 * y;
+            if (i <= c && c < d) Rs[pk(i, c, d)] = g[x][y] * ri[i];
+          }
       }
+      if (jf < d && tid == 0 && !fail) fail = jf + 1;
       __syncthreads();
       if (fail) {
         if (tid == 0) {
@@ -316,80 +398,11 @@ __global__ void __launch_bounds__(NT, 1) cond_kernel(Args a) {
         }
       } else {
         stamp();
-        // ---- blocked inverse X = R^-1 (upper): acc = I; panels from the bottom: (a) one warp finalises the
-        // panel rows by back substitution inside the panel, (b) all warps subtract the panel's contribution
-        // from the rows above: acc[r][c] -= sum_{l in panel} R[r][l] X[l][c]
-        for (int e = tid; e < T; e += NT) Xs[e] = 0.0;
+        // R_k^-1 is formed grid-parallel in phase 3b (one warp per column); hand over 1 / R[p][p] in a.G
+        for (int i = tid; i < d; i += NT) a.G[i] = cs[i];
         __syncthreads();
-        for (int i = tid; i < d; i += NT) Xs[pk(i, i, d)] = 1.0;
-        __syncthreads();
-        const int last = ((d - 1) / NB) * NB;
-        for (int pr = last; pr >= 0; pr -= NB) {
-          const int pn = min(NB, d - pr);
-          if (warp == 0) {   // panel rows pr .. pr+pn-1 of acc in registers; back substitution inside the panel
-            double x[NB][4];
-#pragma unroll
-            for (int q = 0; q < NB; ++q)
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int c = lane + 32 * k, i = pr + q;
-                x[q][k] = (q < pn && c >= i && c < d) ? Xs[pk(i, c, d)] : 0.0;
-              }
-#pragma unroll
-            for (int p = NB - 1; p >= 0; --p) {
-              if (p < pn) {
-                const int i = pr + p;
-#pragma unroll
-                for (int l = p + 1; l < NB; ++l)
-                  if (l < pn) {
-                    const double rl = Gs[pk(i, pr + l, d)];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) x[p][k] = fma(-rl, x[l][k], x[p][k]);
-                  }
-                const double di = dinv[i];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) x[p][k] *= di;
-              }
-            }
-#pragma unroll
-            for (int q = 0; q < NB; ++q)
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int c = lane + 32 * k, i = pr + q;
-                if (q < pn && c >= i && c < d) Xs[pk(i, c, d)] = x[q][k];
-              }
-          }
-          __syncthreads();
-          if (pr > 0) {
-            double Xp[NB][4];
-#pragma unroll
-            for (int q = 0; q < NB; ++q)
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int c = lane + 32 * k, l = pr + q;
-                Xp[q][k] = (q < pn && c >= l && c < d) ? Xs[pk(l, c, d)] : 0.0;
-              }
-            for (int r = warp; r < pr; r += NW) {
-              double f[NB];
-#pragma unroll
-              for (int q = 0; q < NB; ++q) f[q] = q < pn ? Gs[pk(r, pr + q, d)] : 0.0;
-              double* xr = Xs + pk(r, r, d) - r;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int c = lane + 32 * k;
-                if (c >= pr && c < d) {
-                  double v = xr[c];
-#pragma unroll
-                  for (int q = 0; q < NB; ++q) v = fma(-f[q], Xp[q][k], v);
-                  xr[c] = v;
-                }
-              }
-            }
-          }
-          __syncthreads();
-        }
         stamp();
-        for (int e = tid; e < T; e += NT) { a.Rk[e] = Gs[e]; a.Rki[e] = Xs[e]; }
+        for (int e = tid; e < T; e += NT) a.Rk[e] = Rs[e];
         if (tid == 0) a.state[1] = 0;
       }
     }
@@ -398,6 +411,75 @@ __global__ void __launch_bounds__(NT, 1) cond_kernel(Args a) {
     const int st1 = ((volatile int*)a.state)[1];
     if (st1 == 2) break;                                                            // failed even with the shift
     if (st1 == 1) { shifted = 1; npass = 3; pass = -1; Rci = nullptr; continue; }   // restart: shifted CholeskyQR3
+    // ================= phase 3b (all CTAs, after a Cholesky): X = R_k^-1 column by column, one warp per column c
+    // (R X[:, c] = e_c by backward substitution: lane l keeps the partial sums of rows l + 32 k; step p finalises
+    // X[p][c] = s_p / R[p][p], broadcasts it, and the lanes subtract R[r][p] X[p][c] for r < p); R_k staged in
+    // shared memory by every CTA that owns a column
+    if (!near) {
+      const int c = blockIdx.x * NW + warp;
+      if (blockIdx.x * NW < d) {
+        double* sR = sm;       // packed [T]
+        double* sD = sm + T;   // [d] 1 / R[p][p]
+        for (int e = tid; e < T; e += NT) sR[e] = a.Rk[e];
+        for (int i = tid; i < d; i += NT) sD[i] = a.G[i];
+        __syncthreads();
+        if (c < d) {
+          constexpr int KR = FCT_MAX_D / 32;
+          double sv[KR];
+          int rb[KR];   // pk(r, r) - r: R[r][p] = sR[rb + p]
+#pragma unroll
+          for (int k = 0; k < KR; ++k) {
+            const int r = lane + 32 * k;
+            sv[k] = r == c ? 1.0 : 0.0;
+            rb[k] = r < d ? pk(r, r, d) - r : 0;
+          }
+          const long long ck0 = clock64();
+          // branch-free steps (selects only): the loads of R[.][p] do not depend on the chain and are issued first
+          // (one step ahead), so a step costs the SHFL -> DMUL -> DFMA chain
+          double rv[KR], dp = sD[c];
+#pragma unroll
+          for (int k = 0; k < KR; ++k) {
+            const int r = lane + 32 * k;
+            rv[k] = sR[r < c ? rb[k] + c : 0];
+          }
+          for (int p = c; p >= 0; --p) {
+            double rn[KR];
+            const int pn = p > 0 ? p - 1 : 0;
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+              const int r = lane + 32 * k;
+              rn[k] = sR[r < pn ? rb[k] + pn : 0];
+            }
+            const double dn = sD[pn];
+            const int kp = p >> 5;
+            double own = sv[0];
+#pragma unroll
+            for (int k = 1; k < KR; ++k) own = k == kp ? sv[k] : own;
+            const double xp = __shfl_sync(0xffffffffu, own, p & 31) * dp;   // X[p][c]
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+              const int r = lane + 32 * k;
+              const double f = r < p ? rv[k] : 0.0;
+              const double v = fma(-f, xp, sv[k]);
+              sv[k] = r == p ? xp : v;
+              rv[k] = rn[k];
+            }
+            dp = dn;
+          }
+          if (a.ts && c == d - 1 && lane == 0) {   // diagnostics (FCT_COND_TIMING): cycles of the longest column
+            a.ts[60] = (unsigned long long)(clock64() - ck0);
+            a.ts[61] = (unsigned long long)(c + 1);
+          }
+#pragma unroll
+          for (int k = 0; k < KR; ++k) {
+            const int r = lane + 32 * k;
+            if (r <= c) a.Rki[pk(r, c, d)] = sv[k];
+          }
+        }
+      }
+      grid.sync();
+      stamp();
+    }
     // ================= phase 4 (all CTAs): after pass p the cumulative factors live in C[p & 1], Ci[p & 1]
     {
       const int pp = pass & 1;
@@ -451,7 +533,7 @@ int cond_grid() {
 size_t cond_smem(int d) {
   const size_t DP = (size_t)(d + 3) / 4 * 4, T = (size_t)d * (d + 1) / 2;
   const size_t p1 = (size_t)d * DP + 2 * (size_t)ROWS * DP;
-  return sizeof(double) * std::max(std::max(p1, 2 * T), (size_t)NW * 32);
+  return sizeof(double) * std::max(std::max(p1, 2 * T + 3 * 16 * (size_t)NBLK_MAX), (size_t)NW * 32);
 }
 
 size_t ntile_of(int64_t d) {
@@ -493,16 +575,20 @@ extern "C" fct_status fct_condition(const float* Y, int32_t r1, int64_t d, doubl
   a.state = cv.take<int>(4);
   unsigned long long* ts = cv.take<unsigned long long>(64);
   a.ts = getenv("FCT_COND_TIMING") ? ts : nullptr;
+  a.series = getenv("FCT_COND_NOSERIES") ? 0 : 1;
   a.R = R; a.Rinv = Rinv; a.info = info;
   FCT_CUDA_RET(cudaMemsetAsync(a.state, 0, 4 * sizeof(int), st));
   const size_t smem = cond_smem((int)d);
-  static size_t smem_set = 0;
-  if (smem > smem_set) {
-    FCT_CUDA_RET(cudaFuncSetAttribute(cond_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    smem_set = smem;
+  const int nblk = d <= 16 ? 1 : d <= 32 ? 2 : d <= 64 ? 4 : 8;
+  auto kern = nblk == 1 ? cond_kernel<1> : nblk == 2 ? cond_kernel<2> : nblk == 4 ? cond_kernel<4> : cond_kernel<8>;
+  static size_t smem_set[4] = {0, 0, 0, 0};
+  const int ki = nblk == 1 ? 0 : nblk == 2 ? 1 : nblk == 4 ? 2 : 3;
+  if (smem > smem_set[ki]) {
+    FCT_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_set[ki] = smem;
   }
   void* args[] = {&a};
-  FCT_CUDA_RET(cudaLaunchCooperativeKernel((const void*)cond_kernel, dim3(grid), dim3(NT), args, smem, st));
+  FCT_CUDA_RET(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(NT), args, smem, st));
   FCT_LAUNCHED("cond_kernel", st);
   return FCT_OK;
 }

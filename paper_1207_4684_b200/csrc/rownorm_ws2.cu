@@ -174,19 +174,24 @@ struct Smem {   // byte offsets inside the 1024-aligned dynamic shared memory
   int a, b, m64, cm, nrm, cq, bars, total;
 };
 constexpr int kCQ = 4;   // candidate-descriptor ring (selection -> recompute warps)
-// fp64 M for the exact candidate recompute: in shared memory by default; FCT_ROWNORM_M64G=1 reads it through L1
-// from global memory instead (14 KB at d = 64, k = 27), so that the shared memory holds one more tile buffer
+// fp64 M for the exact candidate recompute in shared memory (14 KB at d = 64, k = 27).  Reading it through L1
+// from global memory instead frees one more tile buffer but measured no faster (2.158 vs 2.169 ms per 2^24 rows,
+// profiles/r02_k2_experiments.txt); a runtime choice between the two costs generic (non-LDS) loads
+constexpr bool kM64Smem = true;
 
 // FCT_ROWNORM_DIAG bit 3 (diagnostics only): per-warp cycles spent in mbarrier waits and in total, CTA 0
 __device__ unsigned long long g_rn_prof[32][2];
 __device__ unsigned long long g_rn_cta[1024][2];
-// FCT_ROWNORM_DIAG bit 4 (diagnostics only): CTA-0 timeline of the first kTrace tiles, clock64 per event:
+// FCT_ROWNORM_DIAG bit 4 (diagnostics only, with kTraceBuild): CTA-0 timeline of the first kTrace tiles, clock64 per event:
 // 0 TMA issued, 1 split start, 2 split done, 3 MMA start, 4 MMA committed, 5 epilogue start (max over warps),
 // 6 epilogue done (max over warps), 7 selection done (max over warps)
+// compiled in only when kTraceBuild is set (rebuild to use it): the runtime check alone costs ~2 % at cfg 4
+constexpr bool kTraceBuild = false;
 constexpr int kTrace = 256;
 __device__ unsigned long long g_rn_trace[kTrace][8];
 __device__ __forceinline__ void trace(bool on, int i, int ev) {
-  if (on && blockIdx.x == 0 && i < kTrace && (threadIdx.x & 31) == 0) atomicMax(&g_rn_trace[i][ev], (unsigned long long)clock64());
+  if (kTraceBuild && on && blockIdx.x == 0 && i < kTrace && (threadIdx.x & 31) == 0)
+    atomicMax(&g_rn_trace[i][ev], (unsigned long long)clock64());
 }   // per-CTA globaltimer at start / end (FCT_ROWNORM_PROF)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -234,16 +239,16 @@ __global__ void __launch_bounds__(32 * (kEpiWarp0 + 4 * EG + 4 * RG), 1)
 rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ A, int64_t n, int d, int64_t lda,
                    const float* __restrict__ M32g, int KP32, const double* __restrict__ M64g,
                    const float* __restrict__ colbg, float gam, int NA, int ND, float* __restrict__ lambda,
-                   double* __restrict__ partial, int diag, unsigned whint, int m64s) {
+                   double* __restrict__ partial, int diag, unsigned whint) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* base = smraw + ((1024u - (tcx::su32(smraw) & 1023u)) & 1023u);
   const int dd = D ? D : d;
   const int nch = (dd + 31) >> 5, KP = nch * 32;
   const int tile_floats = nch * 128 * 32;
-  const Smem L = layout(dd, KK, NA, ND, RG > 0, m64s != 0);
+  const Smem L = layout(dd, KK, NA, ND, RG > 0, kM64Smem);
   float* sA = (float*)(base + L.a);
   float* sB = (float*)(base + L.b);
-  const double* M64 = m64s ? (const double*)(base + L.m64) : M64g;
+  const double* M64 = kM64Smem ? (const double*)(base + L.m64) : M64g;
   float* cm = (float*)(base + L.cm);
   float* norms = (float*)(base + L.nrm);
   uint64_t* tma_full = (uint64_t*)(base + L.bars);   // [NA]  tile landed
@@ -294,7 +299,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
     const float hi = tcx::trunc_tf32(m);
     sB[(l >> 5) * 64 * 32 + jj * 32 + ((((l & 31) >> 2) ^ (jj & 7)) << 2) + (l & 3)] = jj < 32 ? hi : m - hi;
   }
-  if (m64s)
+  if (kM64Smem)
     for (int e = tid; e < KK * dd; e += blockDim.x) ((double*)(base + L.m64))[e] = M64g[e];
   for (int e = tid; e < 32; e += blockDim.x) cm[e] = e < KK ? colbg[2 * e] : 0.f;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -555,7 +560,7 @@ fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M3
   // from TMEM (TS form) when it fits next to EG + 1 accumulators.
   const bool at = 4 * KP + 64 * (EG + 1) <= 512 && getenv("FCT_ROWNORM_ATS");
   const int ND = std::min(8, (512 - 2 * (at ? 2 * KP : KP)) / 64);
-  const bool m64s = !getenv("FCT_ROWNORM_M64G");
+  const bool m64s = kM64Smem;
   int NA = 0;
   for (int na = 8; na >= 2; --na)
     if (layout(d, KK, na, ND, RG > 0, m64s).total + 1024 <= (int)kSmemMax - 2048) { NA = na; break; }
@@ -582,7 +587,7 @@ fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M3
   }
   const char* wh = getenv("FCT_WAIT_HINT");
   kern<<<g, threads, smem, st>>>(map, A, n, d, lda, M32, KP32, M64, colb, gam, NA, ND, lambda, partial, diag,
-                                 wh ? (unsigned)atoi(wh) : 20000u, m64s ? 1 : 0);
+                                 wh ? (unsigned)atoi(wh) : 20000u);
   FCT_LAUNCHED("rownorm_ws2_kernel", st);
   fct::set_instance(1, "rownorm_ws2_kernel<%d, %d, %d, %d, %d, %d>", KK, D, EG, RG, keep ? 1 : 0, at ? 1 : 0);
   if (diag & 16) {

@@ -186,6 +186,25 @@ def test_condition_shapes(fct, r1, d):
     assert np.abs(Rinv - Rinv_o).max() <= 1e-12 * cond * np.abs(Rinv_o).max()
 
 
+@pytest.mark.parametrize("r1,d", [(64, 8), (1024, 32), (4096, 64), (8192, 100), (300, 128)])
+def test_condition_series_pass_equals_cholesky_pass(fct, r1, d, monkeypatch):
+    """Passes >= 1 factor a near-identity Gram (|G - I| <= 2^-26 entrywise) by its second-order series
+    (R32) instead of d serial Cholesky steps: R and R^-1 agree with the serial path
+    (FCT_COND_NOSERIES=1) to fp64 rounding, and both match Householder QR."""
+    Y = np.random.default_rng(r1 * 7 + d).standard_normal((r1, d)).astype(np.float32)
+    R_s, Ri_s, info_s = fct.fct_condition(dev(Y))
+    monkeypatch.setenv("FCT_COND_NOSERIES", "1")
+    R_c, Ri_c, info_c = fct.fct_condition(dev(Y))
+    assert int(info_s.item()) == 0 and int(info_c.item()) == 0
+    R_s, Ri_s, R_c, Ri_c = (t.cpu().numpy() for t in (R_s, Ri_s, R_c, Ri_c))
+    assert np.abs(R_s - R_c).max() <= 64 * d * 2.0 ** -53 * np.abs(R_c).max()
+    assert np.abs(Ri_s - Ri_c).max() <= 64 * d * 2.0 ** -53 * np.abs(Ri_c).max()
+    R_o, Rinv_o, _ = oracle.condition(Y.astype(np.float64))
+    cond = np.linalg.cond(Y.astype(np.float64))
+    assert np.abs(R_s - R_o).max() <= 1e-12 * cond * np.abs(R_o).max()
+    assert np.abs(Ri_s - Rinv_o).max() <= 1e-12 * cond * np.abs(Rinv_o).max()
+
+
 # ---------------------------------------------------------------- K2 row-norm
 def _rinv_for(inp):
     """Rinv from the oracle's own conditioning of the oracle sketch (stage-wise parity input)."""

@@ -32,6 +32,8 @@ for r1, d in [(64, 8), (256, 16), (1024, 32), (4096, 64), (8192, 100), (8192, 12
         ws = api.workspace(0, "condition")
         nb = api._lib_().fct_condition_workspace_bytes(r1, d)
         ts_raw = ws.view(torch.uint8)[nb - 512:nb].view(torch.int64).cpu().numpy()
-        out[-1]["phase_us"] = [round((int(b) - int(a_)) / 1e3, 2) for a_, b in zip(ts_raw, ts_raw[1:]) if b > a_]
+        out[-1]["phase_us"] = [round((int(b) - int(a_)) / 1e3, 2) for a_, b in zip(ts_raw[:56], ts_raw[1:56]) if b > a_]
+        if ts_raw[61] > 0:
+            out[-1]["inverse_cycles_per_step"] = round(int(ts_raw[60]) / int(ts_raw[61]), 1)
         print(json.dumps(out[-1]), flush=True)
     print(json.dumps(out[-1]), flush=True)
