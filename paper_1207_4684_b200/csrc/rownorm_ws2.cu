@@ -158,14 +158,36 @@ __device__ __forceinline__ bool certify(const uint32_t (&dv)[32], float n2, cons
   return true;
 }
 
-// fp64 half: exact values of the 1-2 candidates of a descriptor, ranked
+// fp64 half: exact values of the 1-2 candidates of a descriptor, ranked.  One loop for both cases (the second
+// column's loads and FMAs predicated): a warp whose rows mix one- and two-candidate descriptors would otherwise run
+// a one-column and a two-column pass back to back (3 columns of conversions, loads and FMAs instead of 2)
 template <int KK, int D, bool KEEP>
 __device__ __forceinline__ float resolve(uint32_t desc, const float* __restrict__ tile, const float* __restrict__ grow,
                                          int r, int d, const double* __restrict__ M64) {
-  const int j0 = desc & 31, j1 = (desc >> 5) & 31, q1 = (desc >> 10) & 31, q2 = (desc >> 15) & 31;
-  if (!((desc >> 20) & 1u)) return (float)exact_one<KK, D, KEEP>(tile, grow, r, d, M64, j0);
-  double c0, c1;
-  exact_pair<KK, D, KEEP>(tile, grow, r, d, M64, j0, j1, c0, c1);
+  const int j0 = desc & 31, q1 = (desc >> 10) & 31, q2 = (desc >> 15) & 31;
+  const bool two = (desc >> 20) & 1u;
+  const int j1 = two ? (int)((desc >> 5) & 31) : j0;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+  const int dd = D ? D : d;
+#pragma unroll 4
+  for (int l = 0; l < dd; l += 4) {
+    const float4 a = KEEP ? *(const float4*)(tile + tcx::sw_off(r, l)) : __ldg((const float4*)(grow + l));
+    const double d0 = a.x, d1 = a.y, d2 = a.z, d3 = a.w;
+    const double* m = M64 + (size_t)l * KK;
+    a0 = fma(d0, m[j0], a0);
+    a1 = fma(d1, m[KK + j0], a1);
+    a2 = fma(d2, m[2 * KK + j0], a2);
+    a3 = fma(d3, m[3 * KK + j0], a3);
+    if (two) {
+      b0 = fma(d0, m[j1], b0);
+      b1 = fma(d1, m[KK + j1], b1);
+      b2 = fma(d2, m[2 * KK + j1], b2);
+      b3 = fma(d3, m[3 * KK + j1], b3);
+    }
+  }
+  const double c0 = fabs((a0 + a1) + (a2 + a3));
+  if (!two) return (float)c0;
+  const double c1 = fabs((b0 + b1) + (b2 + b3));
   const double cmin = fmin(c0, c1), cmax = fmax(c0, c1);
   return (float)(0.5 * ((q1 == 0 ? cmin : cmax) + (q2 == 0 ? cmin : cmax)));
 }
@@ -555,10 +577,10 @@ fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M3
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   FCT_CHECK_ARG(cr == CUDA_SUCCESS, FCT_ERR_CUDA, "l1_rownorm: cuTensorMapEncodeTiled failed (%d)", (int)cr);
   const int nch = (d + 31) / 32, KP = nch * 32;
-  // A_hi from shared memory (SS form, default): the TMEM it would take holds 6 instead of 4 accumulators at
-  // d = 64, measured 1.0 % faster at cfg 4 (7.50 vs 7.57 ms) and 0.6 % at cfg 3.  FCT_ROWNORM_ATS=1 feeds A_hi
-  // from TMEM (TS form) when it fits next to EG + 1 accumulators.
-  const bool at = 4 * KP + 64 * (EG + 1) <= 512 && getenv("FCT_ROWNORM_ATS");
+  // A_hi from TMEM (TS form, default where it fits next to EG + 1 accumulators): with the single-pass candidate
+  // recompute measured 2 % faster at cfg 4 (6.59 vs 6.73 ms; before it, SS was 1 % faster: 7.50 vs 7.57).
+  // FCT_ROWNORM_SS=1 feeds A_hi from the shared tile (SS form) instead.
+  const bool at = 4 * KP + 64 * (EG + 1) <= 512 && !getenv("FCT_ROWNORM_SS");
   const int ND = std::min(8, (512 - 2 * (at ? 2 * KP : KP)) / 64);
   const bool m64s = kM64Smem;
   int NA = 0;

@@ -454,13 +454,13 @@ def test_rownorm_simt_path_matches_too(fct, c, monkeypatch):
 
 
 @pytest.mark.parametrize("env", ["FCT_ROWNORM_WS1", "FCT_ROWNORM_EG2", "FCT_ROWNORM_NOKEEP", "FCT_ROWNORM_VAR=0",
-                                 "FCT_ROWNORM_ATS", None])
+                                 "FCT_ROWNORM_SS", "FCT_ROWNORM_SS FCT_ROWNORM_EG2", None])
 @pytest.mark.parametrize("c", [2, 4, 5])
 def test_rownorm_tc_variants(fct, c, env, monkeypatch):
     """Each tcgen05 row-norm variant (ws2 with 3 or 2 epilogue groups, the older ws) is parity-green,
     including special rows: zero, tiny (norm underflows in fp32), huge, and a row with exact ties."""
-    if env:
-        k, _, v = env.partition("=")
+    for e in (env or "").split():
+        k, _, v = e.partition("=")
         monkeypatch.setenv(k, v or "1")
     cfg = fctgen.CONFIGS[c]
     inp = fctgen.make_inputs(cfg, n=2 * cfg.s)
