@@ -585,7 +585,7 @@ fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M3
   const bool m64s = kM64Smem;
   int NA = 0;
   for (int na = 8; na >= 2; --na)
-    if (layout(d, KK, na, ND, RG > 0, m64s).total + 1024 <= (int)kSmemMax - 2048) { NA = na; break; }
+    if (layout(d, KK, na, ND, RG > 0, m64s).total + 1024 <= (int)kSmemMax - 512) { NA = na; break; }   // static: < 256 B
   if (NA < 2 || ND < EG + 1) return FCT_ERR_UNSUPPORTED;
   // keep the tile until the epilogue is done (exact recompute from shared memory) when enough buffers fit
   const bool keep = NA >= EG + 2 && !getenv("FCT_ROWNORM_NOKEEP");
