@@ -35,16 +35,15 @@ struct CSwap2 {
   }
 };
 
-// exact |sum_l a_l M_lj| for one or two columns j0, j1 in fp64.  Row: KEEP -> row r of the swizzled shared
-// tile, else the row in global memory.  D = d at compile time (0: runtime d); d % 4 == 0.
+// exact |sum_l a_l M_lj| for two columns j0, j1 in fp64.  Row: KEEP -> row r of the swizzled shared tile, else
+// the row in global memory (L2: five 16-B loads in flight per chunk, the next chunk's loads issued before this
+// chunk's FMAs).  D = d at compile time (0: runtime d); d % 4 == 0.
 template <int KK, int D, bool KEEP>
 __device__ __forceinline__ void exact_pair(const float* __restrict__ tile, const float* __restrict__ grow, int r, int d,
                                           const double* __restrict__ M64, int j0, int j1, double& x0, double& x1) {
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
   const int dd = D ? D : d;
-#pragma unroll 4
-  for (int l = 0; l < dd; l += 4) {
-    const float4 a = KEEP ? *(const float4*)(tile + tcx::sw_off(r, l)) : __ldg((const float4*)(grow + l));
+  auto step = [&](const float4 a, int l) {
     const double d0 = a.x, d1 = a.y, d2 = a.z, d3 = a.w;
     const double* m = M64 + (size_t)l * KK;
     a0 = fma(d0, m[j0], a0);
@@ -55,26 +54,60 @@ __device__ __forceinline__ void exact_pair(const float* __restrict__ tile, const
     b1 = fma(d1, m[KK + j1], b1);
     b2 = fma(d2, m[2 * KK + j1], b2);
     b3 = fma(d3, m[3 * KK + j1], b3);
+  };
+  if constexpr (!KEEP && D > 0 && D % 20 == 0) {
+    float4 q[5];
+#pragma unroll
+    for (int t = 0; t < 5; ++t) q[t] = __ldg((const float4*)(grow + 4 * t));
+#pragma unroll 1
+    for (int l0 = 0; l0 < D; l0 += 20) {
+      float4 nx[5];
+      const int ln = l0 + 20 < D ? l0 + 20 : l0;   // last chunk: harmless reload
+#pragma unroll
+      for (int t = 0; t < 5; ++t) nx[t] = __ldg((const float4*)(grow + ln + 4 * t));
+#pragma unroll
+      for (int t = 0; t < 5; ++t) step(q[t], l0 + 4 * t);
+#pragma unroll
+      for (int t = 0; t < 5; ++t) q[t] = nx[t];
+    }
+  } else {
+#pragma unroll 4
+    for (int l = 0; l < dd; l += 4)
+      step(KEEP ? *(const float4*)(tile + tcx::sw_off(r, l)) : __ldg((const float4*)(grow + l)), l);
   }
   x0 = fabs((a0 + a1) + (a2 + a3));
   x1 = fabs((b0 + b1) + (b2 + b3));
 }
 
-// rare: several candidates -- exact value of each, then rank by counting (ties broken by index); out of line
+// rare: several candidates -- exact value of each, then rank by counting (ties broken by index); out of line.
+// Two candidate columns per pass over the row (ceil(nc/2) passes instead of nc: at the cfg-5 geometry the row comes
+// from L2 and 0.55 % of the rows have nc > 2).  The pending-column form keeps the caller free of spills.
 template <int KK, int D, bool KEEP>
 __device__ __noinline__ void rare_candidates(const float* __restrict__ tile, const float* __restrict__ grow, int r, int d,
                                              const double* __restrict__ M64, unsigned cmask, int q1, int q2, double& x1,
                                              double& x2) {
   double ex[KK];
   x1 = x2 = 0.0;
+  int pend = -1;
 #pragma unroll 1
   for (int j = 0; j < KK; ++j) {
     ex[j] = 0.0;
     if ((cmask >> j) & 1u) {
-      double c0, c1;
-      exact_pair<KK, D, KEEP>(tile, grow, r, d, M64, j, j, c0, c1);
-      ex[j] = c0;
+      if (pend < 0) {
+        pend = j;
+      } else {
+        double c0, c1;
+        exact_pair<KK, D, KEEP>(tile, grow, r, d, M64, pend, j, c0, c1);
+        ex[pend] = c0;
+        ex[j] = c1;
+        pend = -1;
+      }
     }
+  }
+  if (pend >= 0) {
+    double c0, c1;
+    exact_pair<KK, D, KEEP>(tile, grow, r, d, M64, pend, pend, c0, c1);
+    ex[pend] = c0;
   }
 #pragma unroll 1
   for (int a = 0; a < KK; ++a) {
@@ -86,31 +119,16 @@ __device__ __noinline__ void rare_candidates(const float* __restrict__ tile, con
   }
 }
 
-// exact |sum_l a_l M_lj| for one column j (fp64)
-template <int KK, int D, bool KEEP>
-__device__ __forceinline__ double exact_one(const float* __restrict__ tile, const float* __restrict__ grow, int r, int d,
-                                            const double* __restrict__ M64, int j) {
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  const int dd = D ? D : d;
-#pragma unroll 4
-  for (int l = 0; l < dd; l += 4) {
-    const float4 a = KEEP ? *(const float4*)(tile + tcx::sw_off(r, l)) : __ldg((const float4*)(grow + l));
-    const double* m = M64 + (size_t)l * KK + j;
-    a0 = fma((double)a.x, m[0], a0);
-    a1 = fma((double)a.y, m[KK], a1);
-    a2 = fma((double)a.z, m[2 * KK], a2);
-    a3 = fma((double)a.w, m[3 * KK], a3);
-  }
-  return fabs((a0 + a1) + (a2 + a3));
-}
-
-// Selection half of the certified median (no fp64 work unless the row is degenerate): returns true with
-// lam set when the row is settled here (1-2 candidates are handed on as a descriptor otherwise):
-//   desc = j0 | j1 << 5 | q1 << 10 | q2 << 15 | (nc - 1) << 20
-template <int KK, int D, bool KEEP>
-__device__ __forceinline__ bool certify(const uint32_t (&dv)[32], float n2, const float* __restrict__ cm, float gam,
-                                        const float* __restrict__ tile, const float* __restrict__ grow, int r, int d,
-                                        const double* __restrict__ M64, float& lam, uint32_t& desc) {
+// Selection half of the certified median (no fp64 work): returns
+//   kSettled  -- never at present (kept for the degenerate cases a caller may settle itself),
+//   kResolve  -- 1-2 candidates, desc = j0 | j1 << 5 | q1 << 10 | q2 << 15 | (nc - 1) << 20,
+//   kRare     -- nc > 2 candidates (or a degenerate row: all k), rmask = the candidate mask, desc = q1 | q2 << 5.
+// Rare rows are not evaluated here: a warp with one of them would stall all 32 lanes on a serial fp64 pass
+// over the row; the caller queues them and evaluates 32 at a time, one per lane (rare_candidates).
+enum { kSettled = 0, kResolve = 1, kRare = 2 };
+template <int KK>
+__device__ __forceinline__ int certify(const uint32_t (&dv)[32], float n2, const float* __restrict__ cm, float gam,
+                                       uint32_t& desc, uint32_t& rmask) {
   constexpr int m1 = (KK - 1) / 2, m2 = KK / 2;
   float v[KK], srt[KK];
   const float g = gam * __fsqrt_ru(n2);
@@ -150,13 +168,54 @@ __device__ __forceinline__ bool certify(const uint32_t (&dv)[32], float n2, cons
   if (nc <= 2) {
     const int j0 = __ffs(cmask) - 1, j1 = 31 - __clz(cmask);
     desc = (uint32_t)j0 | ((uint32_t)j1 << 5) | ((uint32_t)q1 << 10) | ((uint32_t)q2 << 15) | ((uint32_t)(nc - 1) << 20);
-    return false;
+    return kResolve;
   }
-  double x1, x2;
-  rare_candidates<KK, D, KEEP>(tile, grow, r, d, M64, cmask, q1, q2, x1, x2);
-  lam = (float)(0.5 * (x1 + x2));
-  return true;
+  rmask = cmask;
+  desc = (uint32_t)q1 | ((uint32_t)q2 << 5);
+  return kRare;
 }
+
+// Per-warp queue of rare rows, one entry per lane (row, candidate mask, q1 | q2 << 5).  push() appends the rows
+// whose lanes have rare set (flushing first when they do not fit); flush() evaluates every queued row at once, one
+// row per lane, exactly in fp64 from global memory, and writes lambda.  The order in which a warp settles its rows
+// is fixed, so the warp's share of sum(lambda) is reproducible.
+struct RareQueue {
+  uint32_t row = 0, mask = 0, q = 0;
+  int cnt = 0;
+  template <int KK, int D>
+  __device__ __forceinline__ void flush(const float* __restrict__ A, int64_t lda, int d, const double* __restrict__ M64,
+                                        float* __restrict__ lambda, double& local, int lane) {
+    if (lane < cnt) {
+      double x1, x2;
+      rare_candidates<KK, D, false>(nullptr, A + (int64_t)row * lda, 0, d, M64, mask, (int)(q & 31u),
+                                    (int)((q >> 5) & 31u), x1, x2);
+      const float lam = (float)(0.5 * (x1 + x2));
+      lambda[row] = lam;
+      local += (double)lam;
+    }
+    cnt = 0;
+  }
+  template <int KK, int D>
+  __device__ __forceinline__ void push(bool rare, uint32_t r_row, uint32_t r_mask, uint32_t r_q, const float* __restrict__ A,
+                                       int64_t lda, int d, const double* __restrict__ M64, float* __restrict__ lambda,
+                                       double& local, int lane) {
+    const unsigned rb = __ballot_sync(0xFFFFFFFFu, rare);
+    if (!rb) return;
+    const int nr = __popc(rb);
+    if (cnt + nr > 32) flush<KK, D>(A, lda, d, M64, lambda, local, lane);
+    const int k = lane - cnt;
+    const bool mine = k >= 0 && k < nr;
+    const int src = mine ? (int)__fns(rb, 0u, k + 1) : lane;
+    const uint32_t xr = __shfl_sync(0xFFFFFFFFu, r_row, src), xm = __shfl_sync(0xFFFFFFFFu, r_mask, src),
+                   xq = __shfl_sync(0xFFFFFFFFu, r_q, src);
+    if (mine) {
+      row = xr;
+      mask = xm;
+      q = xq;
+    }
+    cnt += nr;
+  }
+};
 
 // fp64 half: exact values of the 1-2 candidates of a descriptor, ranked.  One loop for both cases (the second
 // column's loads and FMAs predicated): a warp whose rows mix one- and two-candidate descriptors would otherwise run
@@ -169,9 +228,7 @@ __device__ __forceinline__ float resolve(uint32_t desc, const float* __restrict_
   const int j1 = two ? (int)((desc >> 5) & 31) : j0;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
   const int dd = D ? D : d;
-#pragma unroll 4
-  for (int l = 0; l < dd; l += 4) {
-    const float4 a = KEEP ? *(const float4*)(tile + tcx::sw_off(r, l)) : __ldg((const float4*)(grow + l));
+  auto step = [&](const float4 a, int l) {
     const double d0 = a.x, d1 = a.y, d2 = a.z, d3 = a.w;
     const double* m = M64 + (size_t)l * KK;
     a0 = fma(d0, m[j0], a0);
@@ -184,6 +241,26 @@ __device__ __forceinline__ float resolve(uint32_t desc, const float* __restrict_
       b2 = fma(d2, m[2 * KK + j1], b2);
       b3 = fma(d3, m[3 * KK + j1], b3);
     }
+  };
+  if constexpr (!KEEP && D > 0 && D % 20 == 0) {   // row from L2: chunked and prefetched as in exact_pair
+    float4 q[5];
+#pragma unroll
+    for (int t = 0; t < 5; ++t) q[t] = __ldg((const float4*)(grow + 4 * t));
+#pragma unroll 1
+    for (int l0 = 0; l0 < D; l0 += 20) {
+      float4 nx[5];
+      const int ln = l0 + 20 < D ? l0 + 20 : l0;
+#pragma unroll
+      for (int t = 0; t < 5; ++t) nx[t] = __ldg((const float4*)(grow + ln + 4 * t));
+#pragma unroll
+      for (int t = 0; t < 5; ++t) step(q[t], l0 + 4 * t);
+#pragma unroll
+      for (int t = 0; t < 5; ++t) q[t] = nx[t];
+    }
+  } else {
+#pragma unroll 4
+    for (int l = 0; l < dd; l += 4)
+      step(KEEP ? *(const float4*)(tile + tcx::sw_off(r, l)) : __ldg((const float4*)(grow + l)), l);
   }
   const double c0 = fabs((a0 + a1) + (a2 + a3));
   if (!two) return (float)c0;
@@ -453,6 +530,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     int sd = g % ND, sa = g % NA, cs = g % kCQ;
     unsigned ph = (unsigned)((g / ND) & 1), pc = (unsigned)((g / kCQ) & 1);
+    RareQueue rq;
     for (int i = g; i < my_tiles; i += EG) {
       wc.wait([&] {
         tcx::bar_wait_sleep(&d_full[sd], ph, whint);
@@ -475,16 +553,29 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
       const int64_t row = (int64_t)(t0 + i * tstep) * 128 + r;
       const float* tile = sA + sa * tile_floats;
       float lam = 0.f;
-      uint32_t desc = 0u;
-      bool fin = true;
+      uint32_t desc = 0u, rmask = 0u;
+      int st = kSettled;
       if (row < n) {
         if (diag >= 2) lam = __uint_as_float(dv[0]) + n2;   // diag (profiling only): no epilogue arithmetic
-        else fin = certify<KK, D, KEEP>(dv, n2, cm, gam, tile, A + row * lda, r, dd, M64, lam, desc);
+        else st = certify<KK>(dv, n2, cm, gam, desc, rmask);
       }
       trace(trc, i, 7);
       if (RG == 0) {
-        if (row < n) {
-          if (!fin) lam = diag == 1 ? 0.f : resolve<KK, D, KEEP>(desc, tile, A + row * lda, r, dd, M64);
+        // rare rows: queued and evaluated 32 at a time (cfg 4: 6.50 -> 5.89 ms, cfg-5 shard 10.6 -> 8.7 ms) where
+        // the registers allow it; with four groups (80 registers) the queue spills in the loop and the rows are
+        // settled in place from the kept tile instead (cfg 3: 2.04 vs 2.99 ms)
+        constexpr bool kDefer = EG <= 3;
+        if (kDefer) {
+          rq.push<KK, D>(st == kRare, (uint32_t)row, rmask, desc, A, lda, dd, M64, lambda, local, lane);
+        } else if (st == kRare) {
+          double x1, x2;
+          rare_candidates<KK, D, KEEP>(tile, A + row * lda, r, dd, M64, rmask, (int)(desc & 31u), (int)((desc >> 5) & 31u),
+                                       x1, x2);
+          lam = (float)(0.5 * (x1 + x2));
+          st = kSettled;
+        }
+        if (row < n && st != kRare) {
+          if (st == kResolve) lam = diag == 1 ? 0.f : resolve<KK, D, KEEP>(desc, tile, A + row * lda, r, dd, M64);
           lambda[row] = lam;
           local += (double)lam;
         }
@@ -492,6 +583,13 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
         trace(trc, i, 6);
         if (KEEP && lane == 0) tcx::bar_arrive(&a_free[sa]);
       } else {
+        if (st == kRare) {   // separate recompute groups: the rare row is settled here
+          double x1, x2;
+          rare_candidates<KK, D, KEEP>(tile, A + row * lda, r, dd, M64, rmask, (int)(desc & 31u), (int)((desc >> 5) & 31u),
+                                       x1, x2);
+          lam = (float)(0.5 * (x1 + x2));
+        }
+        const bool fin = st != kResolve;
         if (i >= kCQ) tcx::bar_wait(&c_free[cs], pc ^ 1u);
         cdesc[cs * 128 + r] = fin ? 0x80000000u : desc;
         clam[cs * 128 + r] = lam;
@@ -505,6 +603,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
       cs += EG;
       while (cs >= kCQ) { cs -= kCQ; pc ^= 1u; }
     }
+    if (RG == 0 && EG <= 3) rq.flush<KK, D>(A, lda, dd, M64, lambda, local, lane);
   } else {
     // ------------------------------------------------------------------ recompute groups (RG > 0)
     const int rw = warp - kEpiWarp0 - 4 * EG;
