@@ -333,12 +333,12 @@ __host__ __device__ inline Smem layout(int d, int KK, int NA, int ND, bool cq, b
 template <bool AT>
 __host__ __device__ inline int abuf_cols(int KP) { return AT ? 2 * KP : KP; }
 
-template <int KK, int D, int EG, int RG, bool KEEP, bool AT>
+template <int KK, int D, int EG, int RG, bool KEEP, bool AT>   // RG: always 0 (recompute groups were removed)
 __global__ void __launch_bounds__(32 * (kEpiWarp0 + 4 * EG + 4 * RG), 1)
 rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ A, int64_t n, int d, int64_t lda,
                    const float* __restrict__ M32g, int KP32, const double* __restrict__ M64g,
                    const float* __restrict__ colbg, float gam, int NA, int ND, float* __restrict__ lambda,
-                   double* __restrict__ partial, int diag, unsigned whint) {
+                   double* __restrict__ partial, int diag, unsigned whint, unsigned* __restrict__ tctr) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* base = smraw + ((1024u - (tcx::su32(smraw) & 1023u)) & 1023u);
   const int dd = D ? D : d;
@@ -357,12 +357,9 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
   uint64_t* d_full = at_free + 2;                     // [ND]  accumulator ready
   uint64_t* n_full = d_full + ND;                     // [ND]  norms written (4 split-warp arrivals)
   uint64_t* d_free = n_full + ND;                     // [ND]  accumulator + norms drained (4 warp arrivals)
-  uint64_t* c_full = d_free + ND;                     // [kCQ] descriptors written (4 selection-warp arrivals)
-  uint64_t* c_free = c_full + kCQ;                    // [kCQ] descriptors consumed (4 recompute-warp arrivals)
-  uint32_t* cdesc = (uint32_t*)(base + L.cq);
-  float* clam = (float*)(cdesc + kCQ * 128);
   constexpr int NWARPS = kEpiWarp0 + 4 * EG + 4 * RG;
   __shared__ uint32_t tbase;
+  __shared__ int tid_a[8], tid_d[8];   // tile index of each tile buffer / accumulator slot (-1: end marker)
   __shared__ double red[NWARPS];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -379,10 +376,6 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
       tcx::bar_init(&d_full[i], 1);
       tcx::bar_init(&n_full[i], 4);
       tcx::bar_init(&d_free[i], 4);
-    }
-    for (int i = 0; i < kCQ; ++i) {
-      tcx::bar_init(&c_full[i], 4);
-      tcx::bar_init(&c_free[i], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -413,26 +406,30 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
   diag &= 7;
   WaitClock wc(prof);
   if (prof && threadIdx.x == 0) g_rn_cta[blockIdx.x][0] = gtimer();
+  // Tile schedule: CTA b starts with tile b; with a counter (tctr) the TMA producer takes each further tile from it
+  // (dynamic: the CTAs end within a tile of each other; static round robin left a 9 % spread of CTA end times at
+  // cfg 4), else tile b + j * gridDim.x.  After its last tile the producer emits EG end markers (-1) through the
+  // same rings, one for each epilogue group, so every role leaves its loop without knowing the count in advance.
   const int ntiles = (int)((n + 127) / 128);
   const int t0 = blockIdx.x, tstep = gridDim.x;
-  const int my_tiles = t0 < ntiles ? (ntiles - 1 - t0) / tstep + 1 : 0;
   double local = 0.0;
 
   if (warp < kSplitWarps) {
     // ------------------------------------------------------------------ split: norms, A pieces -> TMEM
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    int sa = 0, sd = 0;
+    int sa = 0, sd = 0, ends = 0;
     unsigned pa = 0, pd = 0;   // phase parities of the current ring slots
-    for (int i = 0; i < my_tiles; ++i) {
+    for (int i = 0;; ++i) {
       const int sl = i & 1;
       wc.wait([&] { tcx::bar_wait(&tma_full[sa], pa); });
+      const int tile_id = *(volatile int*)&tid_a[sa];
       if (i >= 2) wc.wait([&] { tcx::bar_wait(&at_free[sl], (unsigned)(((i - 2) >> 1) & 1)); });
       trace(trc, i, 1);
       const float* tile = sA + sa * tile_floats;
       const uint32_t tb = tm + lane_off + (uint32_t)(sl * acols);
       float s2 = 0.f, s2b = 0.f;
 #pragma unroll(D ? (D + 31) / 32 : 1)
-      for (int q = 0; q < nch; ++q) {
+      for (int q = 0; q < (tile_id >= 0 ? nch : 0); ++q) {
         uint32_t hi[32], lo[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
@@ -462,20 +459,33 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
       trace(trc, i, 2);
       if (i >= ND) wc.wait([&] { tcx::bar_wait(&d_free[sd], pd ^ 1u); });
       norms[sd * 128 + tid] = s2 + s2b;
+      if (tid == 0) tid_d[sd] = tile_id;
       __syncwarp();
       if (lane == 0) tcx::bar_arrive(&n_full[sd]);
       if (++sa == NA) { sa = 0; pa ^= 1u; }
       if (++sd == ND) { sd = 0; pd ^= 1u; }
+      if (tile_id < 0 && ++ends == EG) break;
     }
   } else if (warp == kTmaWarp) {
     // ------------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      int sa = 0;
+      int sa = 0, ends = 0;
       unsigned pa = 0;
-      for (int j = 0; j < my_tiles; ++j) {
+      for (int j = 0; ends < EG; ++j) {
+        int tile_id = -1;
+        if (!ends) {
+          tile_id = (j == 0 || !tctr) ? t0 + j * tstep : (int)(tstep + atomicAdd(tctr, 1u));
+          if (tile_id >= ntiles) tile_id = -1;
+        }
         if (j >= NA) wc.wait([&] { tcx::bar_wait(&a_free[sa], pa ^ 1u); });
         trace(trc, j, 0);
-        tcx::tma_tile(sA + sa * tile_floats, &tmA, nch, (t0 + j * tstep) * 128, &tma_full[sa]);
+        tid_a[sa] = tile_id;   // published by the arrive below (release) to the split warps and, through them, the MMA
+        if (tile_id >= 0) {
+          tcx::tma_tile(sA + sa * tile_floats, &tmA, nch, tile_id * 128, &tma_full[sa]);
+        } else {
+          tcx::bar_arrive(&tma_full[sa]);
+          ++ends;
+        }
         if (++sa == NA) { sa = 0; pa ^= 1u; }
       }
     }
@@ -486,9 +496,9 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
       constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
       const int ksteps = (dd + 7) >> 3;
       const uint64_t b00 = tcx::sdesc_sw128(sB), a00 = tcx::sdesc_sw128(sA);
-      int sa = 0, sd = 0;
+      int sa = 0, sd = 0, ends = 0;
       unsigned pd = 0;
-      for (int i = 0; i < my_tiles; ++i) {
+      for (int i = 0;; ++i) {
         const int sl = i & 1;
         wc.wait([&] { tcx::bar_wait(&at_full[sl], (unsigned)((i >> 1) & 1)); });   // implies the TMA tile has landed
         if (i >= ND) wc.wait([&] { tcx::bar_wait(&d_free[sd], pd ^ 1u); });
@@ -497,7 +507,8 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
         const uint32_t tD = tm + dcol0 + (uint32_t)(sd * 64);
         const uint32_t tA = tm + (uint32_t)(sl * acols);
         const uint64_t a0 = a00 + (uint64_t)((sa * tile_floats * 4) >> 4);
-        if (diag != 3) {
+        const int tile_id = *(volatile int*)&tid_a[sa];
+        if (tile_id >= 0 && diag != 3) {
           // D = (A_hi + A_lo) [M_hi | M_lo]: every product of the two-term splits, nothing dropped
 #pragma unroll(D ? (D + 7) / 8 : 1)
           for (int ks = 0; ks < ksteps; ++ks) {
@@ -509,16 +520,17 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
           }
         }
 #pragma unroll(D ? (D + 7) / 8 : 1)
-        for (int ks = 0; ks < ksteps; ++ks) {
+        for (int ks = 0; ks < (tile_id >= 0 ? ksteps : 0); ++ks) {
           const uint64_t bd = b00 + (uint64_t)(((ks >> 2) * 8192 + (ks & 3) * 32) >> 4);
           tcx::mma_tf32_ts(tD, tA + (uint32_t)((AT ? KP : 0) + ks * 8), bd, idesc, diag != 3 || ks > 0);
         }
-        tcx::mma_commit(&d_full[sd]);
+        tcx::mma_commit(&d_full[sd]);   // an end marker commits too (arrives once the earlier MMAs are done)
         tcx::mma_commit(&at_free[sl]);
         if (!KEEP) tcx::mma_commit(&a_free[sa]);
         trace(trc, i, 4);
         if (++sa == NA) sa = 0;
         if (++sd == ND) { sd = 0; pd ^= 1u; }
+        if (tile_id < 0 && ++ends == EG) break;
       }
     }
   } else if (warp < kEpiWarp0 + 4 * EG) {
@@ -528,10 +540,10 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
     const int quad = warp & 3;                        // TMEM lane quadrant this warp may access
     const int r = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    int sd = g % ND, sa = g % NA, cs = g % kCQ;
-    unsigned ph = (unsigned)((g / ND) & 1), pc = (unsigned)((g / kCQ) & 1);
+    int sd = g % ND, sa = g % NA;
+    unsigned ph = (unsigned)((g / ND) & 1);
     RareQueue rq;
-    for (int i = g; i < my_tiles; i += EG) {
+    for (int i = g;; i += EG) {
       wc.wait([&] {
         tcx::bar_wait_sleep(&d_full[sd], ph, whint);
         tcx::bar_wait_sleep(&n_full[sd], ph, whint);
@@ -547,10 +559,15 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
         for (int j = 0; j < 32; ++j) dv[j] = __float_as_uint(__uint_as_float(dv[j]) + __uint_as_float(dw[j]));
       }
       const float n2 = norms[sd * 128 + r];
+      const int tile_id = *(volatile int*)&tid_d[sd];
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) tcx::bar_arrive(&d_free[sd]);
-      const int64_t row = (int64_t)(t0 + i * tstep) * 128 + r;
+      if (tile_id < 0) {   // end marker: release the tile buffer slot as for a tile, then leave
+        if (KEEP && lane == 0) tcx::bar_arrive(&a_free[sa]);
+        break;
+      }
+      const int64_t row = (int64_t)tile_id * 128 + r;
       const float* tile = sA + sa * tile_floats;
       float lam = 0.f;
       uint32_t desc = 0u, rmask = 0u;
@@ -560,7 +577,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
         else st = certify<KK>(dv, n2, cm, gam, desc, rmask);
       }
       trace(trc, i, 7);
-      if (RG == 0) {
+      {
         // rare rows: queued and evaluated 32 at a time (cfg 4: 6.50 -> 5.89 ms, cfg-5 shard 10.6 -> 8.7 ms) where
         // the registers allow it; with four groups (80 registers) the queue spills in the loop and the rows are
         // settled in place from the kept tile instead (cfg 3: 2.04 vs 2.99 ms)
@@ -582,56 +599,13 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
         __syncwarp();
         trace(trc, i, 6);
         if (KEEP && lane == 0) tcx::bar_arrive(&a_free[sa]);
-      } else {
-        if (st == kRare) {   // separate recompute groups: the rare row is settled here
-          double x1, x2;
-          rare_candidates<KK, D, KEEP>(tile, A + row * lda, r, dd, M64, rmask, (int)(desc & 31u), (int)((desc >> 5) & 31u),
-                                       x1, x2);
-          lam = (float)(0.5 * (x1 + x2));
-        }
-        const bool fin = st != kResolve;
-        if (i >= kCQ) tcx::bar_wait(&c_free[cs], pc ^ 1u);
-        cdesc[cs * 128 + r] = fin ? 0x80000000u : desc;
-        clam[cs * 128 + r] = lam;
-        __syncwarp();
-        if (lane == 0) tcx::bar_arrive(&c_full[cs]);
       }
       sa += EG;
       while (sa >= NA) sa -= NA;
       sd += EG;
       if (sd >= ND) { sd -= ND; ph ^= 1u; }
-      cs += EG;
-      while (cs >= kCQ) { cs -= kCQ; pc ^= 1u; }
     }
-    if (RG == 0 && EG <= 3) rq.flush<KK, D>(A, lda, dd, M64, lambda, local, lane);
-  } else {
-    // ------------------------------------------------------------------ recompute groups (RG > 0)
-    const int rw = warp - kEpiWarp0 - 4 * EG;
-    const int g = rw >> 2;
-    const int r = (rw & 3) * 32 + lane;
-    int sa = g % NA, cs = g % kCQ;
-    unsigned pc = (unsigned)((g / kCQ) & 1);
-    for (int i = g; i < my_tiles; i += RG) {
-      tcx::bar_wait_sleep(&c_full[cs], pc, whint);
-      const uint32_t desc = cdesc[cs * 128 + r];
-      float lam = clam[cs * 128 + r];
-      __syncwarp();
-      if (lane == 0) tcx::bar_arrive(&c_free[cs]);
-      const int64_t row = (int64_t)(t0 + i * tstep) * 128 + r;
-      if (row < n) {
-        if (!(desc >> 31) && diag != 1) lam = resolve<KK, D, KEEP>(desc, sA + sa * tile_floats, A + row * lda, r, dd, M64);
-        lambda[row] = lam;
-        local += (double)lam;
-      }
-      if (KEEP) {
-        __syncwarp();
-        if (lane == 0) tcx::bar_arrive(&a_free[sa]);
-      }
-      sa += RG;
-      while (sa >= NA) sa -= NA;
-      cs += RG;
-      while (cs >= kCQ) { cs -= kCQ; pc ^= 1u; }
-    }
+    if (EG <= 3) rq.flush<KK, D>(A, lda, dd, M64, lambda, local, lane);
   }
   wc.flush(warp);
   if (prof && threadIdx.x == 0) g_rn_cta[blockIdx.x][1] = gtimer();
@@ -688,7 +662,7 @@ fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M3
   if (NA < 2 || ND < EG + 1) return FCT_ERR_UNSUPPORTED;
   // keep the tile until the epilogue is done (exact recompute from shared memory) when enough buffers fit
   const bool keep = NA >= EG + 2 && !getenv("FCT_ROWNORM_NOKEEP");
-  if (RG > 0 && !keep) return FCT_ERR_UNSUPPORTED;
+  if (RG > 0) return FCT_ERR_UNSUPPORTED;   // separate recompute groups were measured slower and removed
   const size_t smem = (size_t)layout(d, KK, NA, ND, RG > 0, m64s).total + 1024;
   const int g = std::max(1, std::min(grid, fct::num_sms()));
   const int threads = 32 * (kEpiWarp0 + 4 * EG + 4 * RG);
@@ -707,9 +681,14 @@ fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M3
     if (cudaGetSymbolAddress(&tp, g_rn_trace) == cudaSuccess) cudaMemsetAsync(tp, 0, sizeof(unsigned long long) * kTrace * 8, st);
   }
   const char* wh = getenv("FCT_WAIT_HINT");
+  // dynamic tile schedule: the counter lives in the last partial slot (g < grid, zeroed above; reset after the
+  // kernel so the partial sum is unchanged).  FCT_ROWNORM_STATIC=1 keeps the round-robin schedule.
+  const bool dyn = g < grid && !getenv("FCT_ROWNORM_STATIC");
+  unsigned* tctr = dyn ? (unsigned*)(partial + grid - 1) : nullptr;
   kern<<<g, threads, smem, st>>>(map, A, n, d, lda, M32, KP32, M64, colb, gam, NA, ND, lambda, partial, diag,
-                                 wh ? (unsigned)atoi(wh) : 20000u);
+                                 wh ? (unsigned)atoi(wh) : 20000u, tctr);
   FCT_LAUNCHED("rownorm_ws2_kernel", st);
+  if (dyn) FCT_CUDA_RET(cudaMemsetAsync(partial + grid - 1, 0, sizeof(double), st));
   fct::set_instance(1, "rownorm_ws2_kernel<%d, %d, %d, %d, %d, %d>", KK, D, EG, RG, keep ? 1 : 0, at ? 1 : 0);
   if (diag & 16) {
     static unsigned long long tr[kTrace][8];
@@ -775,7 +754,6 @@ fct_status launch_k(const float* A, int64_t n, int d, int64_t lda, const float* 
 #define FCT_RN_LAUNCH(DD)                                                                                  \
   do {                                                                                                     \
     fct_status rc_ = FCT_ERR_UNSUPPORTED;                                                                  \
-    if (var == 0) rc_ = launch<KK, DD, 2, 2>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st); \
     if (rc_ != FCT_ERR_UNSUPPORTED) return rc_;                                                            \
     if (var == 2) return launch<KK, DD, 2, 0>(A, n, d, lda, M32, KP32, M64, colb, partial, grid, lambda, st); \
     if (var == 3) {                                                                                        \
