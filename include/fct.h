@@ -109,7 +109,10 @@ fct_status fct_condition(const float* Y, int32_t r1, int64_t d, double* R, doubl
  * l1 row-norm estimation (Lemma medCauchy, cost P:L2168-2175):
  *     M = Rinv * Pi2 (formed first, fp64);  Lambda = A M;
  *     lambda[i] = median_j |Lambda_ij|   (even k: mean of the two middle order statistics)
- *     *lambda_sum += sum_i lambda[i]      (fp64 device scalar, fixed summation order)
+ *     *lambda_sum += sum_i lambda[i]      (fp64 device scalar)
+ * lambda is deterministic (each entry is the exact median rounded once).  lambda_sum is a sum of per-CTA fp64
+ * partials; the tensor-core kernel hands tiles to CTAs dynamically, so its summation order (and the last bits of
+ * lambda_sum) may vary run to run, as Y does (R20); FCT_ROWNORM_STATIC=1 fixes the order.
  * Rinv: d x d fp64; Pi2: d x k fp32 (i.i.d. Cauchy); lambda: n fp32.
  * Accuracy: |lambda - exact| <= 1e-5 * exact per row.  Rows whose fp32 evaluation cannot be
  * certified to that bound (cancellation) are recomputed in fp64 inside the kernel.
