@@ -91,18 +91,16 @@ __device__ __noinline__ void rare_candidates(const float* __restrict__ tile, con
   x1 = x2 = 0.0;
   int pend = -1;
 #pragma unroll 1
-  for (int j = 0; j < KK; ++j) {
-    ex[j] = 0.0;
-    if ((cmask >> j) & 1u) {
-      if (pend < 0) {
-        pend = j;
-      } else {
-        double c0, c1;
-        exact_pair<KK, D, KEEP>(tile, grow, r, d, M64, pend, j, c0, c1);
-        ex[pend] = c0;
-        ex[j] = c1;
-        pend = -1;
-      }
+  for (unsigned m = cmask; m; m &= m - 1u) {   // candidate columns only (ex[] is read for them only)
+    const int j = __ffs(m) - 1;
+    if (pend < 0) {
+      pend = j;
+    } else {
+      double c0, c1;
+      exact_pair<KK, D, KEEP>(tile, grow, r, d, M64, pend, j, c0, c1);
+      ex[pend] = c0;
+      ex[j] = c1;
+      pend = -1;
     }
   }
   if (pend >= 0) {
@@ -110,11 +108,17 @@ __device__ __noinline__ void rare_candidates(const float* __restrict__ tile, con
     exact_pair<KK, D, KEEP>(tile, grow, r, d, M64, pend, pend, c0, c1);
     ex[pend] = c0;
   }
+  // rank among the candidates only (nc^2 comparisons instead of k^2: at cfg 3 the k^2 loop was 17 % of the
+  // kernel's instructions)
 #pragma unroll 1
-  for (int a = 0; a < KK; ++a) {
-    if (!((cmask >> a) & 1u)) continue;
+  for (unsigned ma = cmask; ma; ma &= ma - 1u) {
+    const int a = __ffs(ma) - 1;
     int rank = 0;
-    for (int b = 0; b < KK; ++b) rank += ((cmask >> b) & 1u) && (ex[b] < ex[a] || (ex[b] == ex[a] && b < a));
+#pragma unroll 1
+    for (unsigned mb = cmask; mb; mb &= mb - 1u) {
+      const int b = __ffs(mb) - 1;
+      rank += ex[b] < ex[a] || (ex[b] == ex[a] && b < a);
+    }
     if (rank == q1) x1 = ex[a];
     if (rank == q2) x2 = ex[a];
   }
@@ -592,7 +596,7 @@ rownorm_ws2_kernel(const __grid_constant__ CUtensorMap tmA, const float* __restr
       {
         // rare rows: queued and evaluated 32 at a time (cfg 4: 6.50 -> 5.89 ms, cfg-5 shard 10.6 -> 8.7 ms) where
         // the registers allow it; with four groups (80 registers) the queue spills in the loop and the rows are
-        // settled in place from the kept tile instead (cfg 3: 2.04 vs 2.99 ms)
+        // settled in place from the kept tile instead
         constexpr bool kDefer = EG <= 3;
         if (kDefer) {
           rq.push<KK, D>(st == kRare, (uint32_t)row, rmask, desc, A, lda, dd, M64, lambda, local, lane);
@@ -758,11 +762,11 @@ fct_status launch(const float* A, int64_t n, int d, int64_t lda, const float* M3
 template <int KK, int DC>
 fct_status launch_k(const float* A, int64_t n, int d, int64_t lda, const float* M32, int KP32, const double* M64,
                     const float* colb, double* partial, int grid, float* lambda, cudaStream_t st) {
-  // variants (FCT_ROWNORM_VAR): 0 = 2 selection + 2 recompute groups, 1 = 3 groups that also recompute,
-  // 2 = 2 groups that also recompute, 3 = 4 groups.  Default 1, and 3 at d = 32 (cfg 3 shape: 2.06 vs
-  // 2.18 ms measured; at d = 64 four groups cost the KEEP buffer and are 21 % slower)
+  // variants (FCT_ROWNORM_VAR): 1 = 3 epilogue groups (default), 2 = 2 groups, 3 = 4 groups.  Four groups were
+  // faster at d = 32 while rare rows were settled in place (2.06 vs 2.18 ms); with the rare-row queue, which needs
+  // the registers of three groups, three are faster there too (cfg 3: 1.06 vs 1.25 ms)
   const char* ve = getenv("FCT_ROWNORM_VAR");
-  const int var = ve ? atoi(ve) : (getenv("FCT_ROWNORM_EG2") ? 2 : (d > 16 && d <= 32 ? 3 : 1));
+  const int var = ve ? atoi(ve) : (getenv("FCT_ROWNORM_EG2") ? 2 : 1);
 #define FCT_RN_LAUNCH(DD)                                                                                  \
   do {                                                                                                     \
     fct_status rc_ = FCT_ERR_UNSUPPORTED;                                                                  \

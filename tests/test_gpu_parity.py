@@ -453,7 +453,7 @@ def test_rownorm_simt_path_matches_too(fct, c, monkeypatch):
     assert (np.abs(lam - lam_o) <= LAM_TOL * lam_o).all()
 
 
-@pytest.mark.parametrize("env", ["FCT_ROWNORM_WS1", "FCT_ROWNORM_EG2", "FCT_ROWNORM_NOKEEP", "FCT_ROWNORM_STATIC",
+@pytest.mark.parametrize("env", ["FCT_ROWNORM_WS1", "FCT_ROWNORM_EG2", "FCT_ROWNORM_NOKEEP", "FCT_ROWNORM_STATIC", "FCT_ROWNORM_VAR=3",
                                  "FCT_ROWNORM_SS", "FCT_ROWNORM_SS FCT_ROWNORM_EG2", None])
 @pytest.mark.parametrize("c", [2, 4, 5])
 def test_rownorm_tc_variants(fct, c, env, monkeypatch):
