@@ -132,6 +132,24 @@ __device__ __forceinline__ void scatter(float* __restrict__ P, const int (&addr)
   }
 }
 
+// the 8 updates of a row group go out in two batches of 4: fewer take/put windows open at once, so fewer collide
+// and take the re-add loop (cfg 4: 9.52 -> 9.31 ms; batches of 2: 9.81 ms; tools/sk_batch.sh)
+constexpr int kScatN = 4;
+template <int MODE>
+__device__ __forceinline__ void scatter8(float* __restrict__ P, const int (&ad)[8], const float (&vv)[8]) {
+#pragma unroll
+  for (int h = 0; h < 8; h += kScatN) {
+    int a2[kScatN];
+    float v2[kScatN];
+#pragma unroll
+    for (int q = 0; q < kScatN; ++q) {
+      a2[q] = ad[h + q];
+      v2[q] = vv[h + q];
+    }
+    scatter<MODE, kScatN>(P, a2, v2);
+  }
+}
+
 template <int LA, int LB, int DT, int TILES_, bool SA_ = false>
 struct Geo5 {
   // SA (shared aux): the identity and Hadamard halves of the aux use ONE pair of buffers in turn (the Hadamard
@@ -277,7 +295,7 @@ sketch_v5_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           ad[q] = hv[q] * DT + c;
           vv[q] = (4.f * cw[q]) * x[k0 + q];
         }
-        scatter<MODE, 8>(P, ad, vv);
+        scatter8<MODE>(P, ad, vv);
       }
       fwht<RA>(x);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -317,7 +335,7 @@ sketch_v5_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           ad[q] = sHh[aux_off(e)] * DT + c;
           vv[q] = (sc_h * sCh[aux_off(e)]) * y[gi][k0 + q];
         }
-        scatter<MODE, 8>(P, ad, vv);
+        scatter8<MODE>(P, ad, vv);
       }
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
