@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(Geo5<LA, LB, DT, TL, SA>::THREADS, 1)
 sketch_v5_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
                  const __grid_constant__ CUtensorMap tmH, const int8_t* __restrict__ signs, int r1, int d,
                  int nslices, int64_t nblocks, float inv_sqrt_s, double* __restrict__ W, int* __restrict__ pace,
-                 int pace_every) {
+                 int pace_every, int64_t nmain, int nextra) {
   using Gm = Geo5<LA, LB, DT, TL, SA>;
   constexpr int S = Gm::S, RA = Gm::RA, RB = Gm::RB, NG = Gm::NG, NT = Gm::NT, NB = Gm::NB, TILES = Gm::TILES,
                 G = Gm::G;
@@ -195,10 +195,17 @@ sketch_v5_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   // static barriers then occupy the first 1 KB of the CTA's shared memory)
   extern __shared__ __align__(1024) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bar_t[TILES], bar_i[TILES], bar_h[TILES];
-  const int cs = blockIdx.x % nslices;
-  const int grp = blockIdx.x / nslices;
-  const int ngrp = gridDim.x / nslices;
-  const int c0 = cs * DT;
+  // Work split (all SMs busy when the slice count does not divide them): the first ngrp * nslices CTAs form ngrp
+  // groups of nslices (one CTA per column slice) over the blocks [0, nmain); the nextra further CTAs (nslices a
+  // multiple of nextra) take the blocks [nmain, nblocks) in nslices / nextra passes, slices e, e + nextra, ...,
+  // flushing P between passes.  nmain is chosen so that both kinds of CTA do the same number of block-slices.
+  const int ngrp = (gridDim.x - nextra) / nslices;
+  const bool extra = (int)blockIdx.x >= ngrp * nslices;
+  const int eidx = extra ? (int)blockIdx.x - ngrp * nslices : 0;
+  const int nseg = extra ? nslices / nextra : 1;
+  const int grp = extra ? ngrp : (int)blockIdx.x / nslices;
+  int cs = extra ? eidx : (int)blockIdx.x % nslices;
+  int c0 = cs * DT;
   const int tg = threadIdx.x / NT;
   const int lt = threadIdx.x - tg * NT;
   const int c = lt % DT;
@@ -238,23 +245,38 @@ sketch_v5_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     tma2((void*)sHh, &tmH, 0, row, &bar_h[tg]);
   };
 
-  const int64_t bstep = (int64_t)ngrp * TILES;
-  int64_t b = grp + (int64_t)ngrp * tg;
-  if (lt == 0 && b < nblocks) {
+  unsigned phase = 0;
+  const float sc_h = 4.f * inv_sqrt_s;
+  for (int seg = 0; seg < nseg; ++seg) {
+  if (seg > 0) {   // extra CTA: flush this slice's partial, then the next slice
+    __syncthreads();
+    for (int e = threadIdx.x; e < r1 * DT; e += blockDim.x) {
+      const int h = e / DT, cc = e - h * DT;
+      const float v = P[e];
+      if (c0 + cc < d && v != 0.f) atomicAdd(&W[(size_t)h * d + c0 + cc], (double)v);
+      P[e] = 0.f;
+    }
+    cs += nextra;
+    c0 = cs * DT;
+    __syncthreads();
+  }
+  const int64_t bstep = extra ? (int64_t)TILES : (int64_t)ngrp * TILES;
+  const int64_t bend = extra ? nblocks : nmain;
+  int64_t b = extra ? nmain + tg : grp + (int64_t)ngrp * tg;
+  const int pidx = extra ? ngrp + seg : grp, parts = extra ? nextra : nslices;
+  if (lt == 0 && b < bend) {
     issue_tile(b);
     issue_id(b);
     if (!SA) issue_had(b);
   }
-  unsigned phase = 0;
-  const float sc_h = 4.f * inv_sqrt_s;
   int it = 0;
-  for (; b < nblocks; b += bstep, ++it) {
+  for (; b < bend; b += bstep, ++it) {
     const int64_t bn = b + bstep;
     // pacing: the nslices CTAs of a row-block group meet every pace_every blocks (a counter in global memory), so
     // the column slices stay in lockstep and each line of A / of the aux is still in L2 when the neighbours read it
     if (pace && tg == 0 && lt == 0 && it > 0 && it % pace_every == 0) {
-      int* cnt = pace + grp;
-      const int want = nslices * (it / pace_every);
+      int* cnt = pace + pidx;
+      const int want = parts * (it / pace_every);
       atomicAdd(cnt, 1);
       int v, spins = 0;   // a soft meeting point: the wait is bounded (~0.4 ms), so it can never deadlock
       do {
@@ -302,7 +324,7 @@ sketch_v5_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       nbar(1 + tg, NT);   // tile and identity aux consumed
       if (lt == 0) {
         if (SA) issue_had(b);                 // the Hadamard half of THIS block into the same buffers
-        else if (bn < nblocks) issue_id(bn);
+        else if (bn < bend) issue_id(bn);
       }
 #pragma unroll
       for (int k = 0; k < RA; ++k) tile[xswz<LA, G>(RA * g + k) * DT + c] = x[k];
@@ -318,7 +340,7 @@ sketch_v5_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     nbar(1 + tg, NT);   // the tile buffer is free: prefetch the next block
-    if (lt == 0 && bn < nblocks) issue_tile(bn);
+    if (lt == 0 && bn < bend) issue_tile(bn);
     mb_wait(&bar_h[tg], phase);
     phase ^= 1u;
 #pragma unroll
@@ -340,11 +362,12 @@ sketch_v5_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     nbar(1 + tg, NT);   // the Hadamard aux is free
-    if (lt == 0 && bn < nblocks) {
+    if (lt == 0 && bn < bend) {
       if (SA) issue_id(bn);
       else issue_had(bn);
     }
   }
+  }   // segments
   __syncthreads();
   for (int e = threadIdx.x; e < r1 * DT; e += blockDim.x) {
     const int h = e / DT, cc = e - h * DT;
@@ -417,8 +440,21 @@ fct_status launch_v5(const float* A, int64_t nfull, int64_t d, int64_t lda, cons
   ngrp = std::min<int64_t>(ngrp, (nblocks + TL - 1) / TL);
   if (ngrp < 1) ngrp = 1;
   if (ngrp * nslices > fct::num_sms()) pace = nullptr;
-  kern<<<(unsigned)(ngrp * nslices), Gm::THREADS, smem, st>>>(mA, mC, mH, signs, r1, (int)d, nslices, nblocks,
-                                                               (float)(1.0 / sqrt((double)s)), W, pace, pace_every);
+  // SMs left over by the groups (cfg 4: 148 - 18 x 8 = 4) take a tail of the blocks in nslices / nextra passes;
+  // the tail is sized so that an extra CTA does as many block-slices as a group CTA (FCT_SKETCH_NOEXTRA=1: off)
+  // (nextra = the largest divisor of nslices that the leftover SMs hold: cfg 5 has 148 - 5 x 25 = 23 left, uses 5)
+  int nextra = (int)(fct::num_sms() - ngrp * nslices);
+  while (nextra > 0 && nslices % nextra) --nextra;
+  int64_t nmain = nblocks;
+  if (nextra > 0 && pace && !getenv("FCT_SKETCH_NOEXTRA")) {
+    const int64_t passes = nslices / nextra;
+    const int64_t tail = nblocks / (1 + passes * ngrp);
+    if (tail >= 4 * TL) nmain = nblocks - tail;
+  }
+  if (nmain == nblocks) nextra = 0;
+  kern<<<(unsigned)(ngrp * nslices + nextra), Gm::THREADS, smem, st>>>(mA, mC, mH, signs, r1, (int)d, nslices, nblocks,
+                                                                       (float)(1.0 / sqrt((double)s)), W, pace, pace_every,
+                                                                       nmain, nextra);
   FCT_LAUNCHED("sketch_v5_kernel", st);
   fct::set_instance(0, "sketch_v5_kernel<%d, %d, %d, %d, %d, %d>", LA, LB, DT, TL, MODE, SA ? 1 : 0);   // ncu's spelling
   return FCT_OK;

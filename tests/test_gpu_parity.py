@@ -80,6 +80,20 @@ def test_sketch_edge_shapes(fct, n, d, s, r1):
     assert_sketch_close(Yg, Yo, Mb)
 
 
+@pytest.mark.parametrize("noextra", [False, True])
+def test_sketch_extra_ctas_tail(fct, noextra, monkeypatch):
+    """K1's leftover SMs (5 slices of 16 columns fill 145 of 148 SMs; the 3 left over run one extra CTA that takes
+    a tail of the blocks in 5 passes, one slice per pass, flushing its partial between passes), with a partly
+    empty last slice (d = 72) and a ragged tail block; the same input with the extra CTAs switched off."""
+    if noextra:
+        monkeypatch.setenv("FCT_SKETCH_NOEXTRA", "1")
+    cfg = fctgen.CONFIGS[2]
+    inp = fctgen.make_inputs(cfg, n=1200 * 256 + 77, s=256, r1=1024, d=72)
+    Yo, Mb = oracle.sketch(inp.A, inp.signs, inp.cauchy, inp.hash, 256, 1024)
+    Yg = sketch_gpu(fct, inp)
+    assert_sketch_close(Yg, Yo, Mb)
+
+
 def test_sketch_strided_accumulate_and_shards(fct):
     """lda > d (a column slice of a wider matrix), accumulate=1, and s-aligned row shards."""
     cfg = fctgen.CONFIGS[2]
