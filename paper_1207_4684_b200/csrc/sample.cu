@@ -146,6 +146,10 @@ __global__ void __launch_bounds__(kThreads) write_kernel(Decide dec, int64_t n, 
 // INCLUSIVE prefix, publishes its own INCLUSIVE prefix and writes its kept rows.  Integer arithmetic
 // only -> idx / weight / count bit-identical to the three-kernel path.  Reads lambda once, writes p once.
 constexpr uint64_t kAgg = 1ull << 62, kInc = 2ull << 62, kValMask = (1ull << 62) - 1;
+// 32 rows per thread, 8192 per tile: the look-back chain (each tile waits for a predecessor's inclusive prefix) was
+// the bound with 2048-row tiles (ncu: 45 % of the stall samples at the barrier behind warp 0's look-back, DRAM
+// throughput 16 %); phat is recomputed for the few kept rows instead of being held for all 32
+constexpr int kFRows = 32, kFTile = kThreads * kFRows;
 
 __global__ void __launch_bounds__(kThreads) probs_sample_kernel(const float* __restrict__ lambda,
                                                                  const double* __restrict__ total, float* __restrict__ p,
@@ -160,32 +164,34 @@ __global__ void __launch_bounds__(kThreads) probs_sample_kernel(const float* __r
   __syncthreads();
   const int64_t tile = s_tile;
   const double tot = *total;
-  const int64_t base = tile * kTile + (int64_t)threadIdx.x * kRowsPerThread;
+  const int64_t base = tile * kFTile + (int64_t)threadIdx.x * kFRows;
   unsigned keep = 0u;
-  double ph[kRowsPerThread];
-  float pv[kRowsPerThread];
-  if (vec && base + kRowsPerThread <= n) {
-    const float4 l0 = *(const float4*)(lambda + base), l1 = *(const float4*)(lambda + base + 4);
-    const float lv[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+  if (vec && base + kFRows <= n) {
 #pragma unroll
-    for (int r = 0; r < kRowsPerThread; ++r) pv[r] = (float)((double)lv[r] / tot);
-    *(float4*)(p + base) = make_float4(pv[0], pv[1], pv[2], pv[3]);
-    *(float4*)(p + base + 4) = make_float4(pv[4], pv[5], pv[6], pv[7]);
-  } else {
+    for (int q = 0; q < kFRows; q += 4) {
+      const float4 l = *(const float4*)(lambda + base + q);
+      const float lv[4] = {l.x, l.y, l.z, l.w};
+      float pv[4];
 #pragma unroll
-    for (int r = 0; r < kRowsPerThread; ++r) {
-      pv[r] = 0.f;
-      if (base + r < n) {
-        pv[r] = (float)((double)lambda[base + r] / tot);
-        p[base + r] = pv[r];
+      for (int r = 0; r < 4; ++r) pv[r] = (float)((double)lv[r] / tot);
+      *(float4*)(p + base + q) = make_float4(pv[0], pv[1], pv[2], pv[3]);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        double ph;
+        if (dec.decide_p(pv[r], base + q + r, ph)) keep |= 1u << (q + r);
       }
     }
-  }
-#pragma unroll
-  for (int r = 0; r < kRowsPerThread; ++r) {
-    const int64_t i = base + r;
-    ph[r] = 1.0;
-    if (i < n && dec.decide_p(pv[r], i, ph[r])) keep |= 1u << r;
+  } else {
+#pragma unroll 4
+    for (int r = 0; r < kFRows; ++r) {
+      const int64_t i = base + r;
+      if (i < n) {
+        const float pv = (float)((double)lambda[i] / tot);
+        p[i] = pv;
+        double ph;
+        if (dec.decide_p(pv, i, ph)) keep |= 1u << r;
+      }
+    }
   }
   const int c = __popc(keep);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -239,15 +245,16 @@ __global__ void __launch_bounds__(kThreads) probs_sample_kernel(const float* __r
   }
   __syncthreads();
   int64_t pos = s_excl + wpre + x - c;
-#pragma unroll
-  for (int r = 0; r < kRowsPerThread; ++r) {
-    if ((keep >> r) & 1u) {
-      if (pos < capacity) {
-        idx[pos] = dec.row_base + base + r;
-        weight[pos] = 1.0 / ph[r];
-      }
-      ++pos;
+  for (unsigned kb = keep; kb; kb &= kb - 1u) {   // kept rows (few): phat again from the same p
+    const int r = __ffs(kb) - 1;
+    if (pos < capacity) {
+      const float pv = (float)((double)lambda[base + r] / tot);
+      double ph;
+      dec.decide_p(pv, base + r, ph);
+      idx[pos] = dec.row_base + base + r;
+      weight[pos] = 1.0 / ph;
     }
+    ++pos;
   }
 }
 
@@ -312,7 +319,7 @@ extern "C" fct_status l1_probs_sample(const float* lambda, int64_t n, const doub
   const size_t need = l1_probs_sample_workspace_bytes(n);
   FCT_CHECK_ARG(workspace && workspace_bytes >= need, FCT_ERR_WORKSPACE, "l1_probs_sample: workspace %zu < %zu bytes",
                 workspace_bytes, need);
-  const int64_t ntiles = (n + kTile - 1) / kTile;
+  const int64_t ntiles = (n + kFTile - 1) / kFTile;
   FCT_CHECK_ARG(ntiles <= 0x7fffffffLL, FCT_ERR_SHAPE, "l1_probs_sample: n too large");
   cudaStream_t st = (cudaStream_t)stream;
   unsigned long long* state = (unsigned long long*)workspace;
