@@ -430,15 +430,14 @@ rownorm_v1_kernel(const float* __restrict__ A, int64_t n, int d, int64_t lda, co
 }
 
 // ------------------------------------------------------------------------------------------------
-// tc: the contraction Lambda = A M on the 5th-generation tensor cores (tcgen05, kind::tf32, 3xTF32):
-//   D = A*M_hi + A*M_lo + A_lo*M_hi,  A_hi = trunc_tf32(A) (the MMA's own operand truncation),
-//   A_lo = A - A_hi (exact in fp32, written to TMEM by the threads), M_hi/M_lo likewise.
-// Tile = 128 rows x Kp (Kp = d rounded up to 32) fp32, TMA-loaded with SWIZZLE_128B (K-major canonical
-// layout for the UMMA descriptor); D (128 x 32 fp32) lives in TMEM; thread t owns row t (TMEM lane t)
-// for the split and for the certified-median epilogue (identical to v1, with the error bound of the
-// 3xTF32 evaluation: measured max |err| = 1.9e-6 * sum|a m| on the box, bound used 2^-14 * 1.05 *
-// min(||a||_2 ||m~_j||_2, ||a||_1 ||m~_j||_inf)).  Double-buffered: the split + MMA of tile i+1 and the
-// TMA of tile i+2 overlap the epilogue of tile i.
+// tc: helpers for the tcgen05 row-norm kernel below (ws; the ws2 kernel in rownorm_ws2.cu is the default for
+// the five configurations' k).  The contraction Lambda = A M runs on the 5th-generation tensor cores
+// (kind::tf32, 3xTF32): D = A*M_hi + A*M_lo + A_lo*M_hi, A_hi = trunc_tf32(A) (the MMA's own operand
+// truncation), A_lo = A - A_hi (exact in fp32, written to TMEM by the threads), M_hi/M_lo likewise.
+// Tiles = 128 rows x Kp (Kp = d rounded up to 32) fp32, TMA-loaded with SWIZZLE_128B (K-major canonical
+// layout for the UMMA descriptor); D lives in TMEM; error bound of the 3xTF32 evaluation: measured max
+// |err| = 1.9e-6 * sum|a m| on the box, bound used 2^-14 * 1.05 * min(||a||_2 ||m~_j||_2, ||a||_1 ||m~_j||_inf).
+// (The single-role double-buffered tc kernel that preceded ws was superseded by it and removed in round 2.)
 namespace tc {
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint64_t sdesc(const void* p) {   // K-major SWIZZLE_128B, SBO = 1024 B
@@ -479,256 +478,7 @@ __device__ __forceinline__ void ld32(uint32_t taddr, uint32_t (&v)[32]) {
                : "memory");
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-// exact |sum_l a_l M_lj| in fp64 for row r of a swizzled tile
-__device__ __forceinline__ double exact_abs_dot_sw(const float* __restrict__ tile, int r, const double* __restrict__ mc,
-                                                   int k, int d) {
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  for (int l = 0; l < d; l += 4) {
-    const int q = l >> 5, c = (l & 31) >> 2;
-    const float4 a = *(const float4*)(tile + q * 128 * 32 + r * 32 + ((c ^ (r & 7)) << 2));
-    s0 = fma((double)a.x, mc[(l + 0) * k], s0);
-    s1 = fma((double)a.y, mc[(l + 1) * k], s1);
-    s2 = fma((double)a.z, mc[(l + 2) * k], s2);
-    s3 = fma((double)a.w, mc[(l + 3) * k], s3);
-  }
-  return fabs((s0 + s1) + (s2 + s3));
-}
 }  // namespace tc
-
-template <int K>
-__device__ __forceinline__ float certified_median_tc(const float (&acc)[K], float n1, float n2,
-                                                     const float* __restrict__ colb, float gam, int k, int m1, int m2,
-                                                     const float* __restrict__ tile, int r, int d,
-                                                     const double* __restrict__ M64) {
-  if (n1 == 0.f) return 0.f;
-  const float nrm2 = __fsqrt_ru(n2) * 1.0001f;
-  float srt[K];
-  float E = 0.f;
-  bool bad = false;
-#pragma unroll
-  for (int j = 0; j < K; ++j) {
-    const float v = fabsf(acc[j]);
-    const float ej = j < k ? gam * fminf(nrm2 * colb[2 * j], n1 * colb[2 * j + 1]) + 1e-37f : 0.f;
-    bad |= !(isfinite(v) && isfinite(ej));
-    E = fmaxf(E, ej);
-    srt[j] = j < k ? v : INFINITY;
-  }
-  switch (K - k) {
-    case 0: selnet<K>(srt, CSwap{}); break;
-    case 1: if constexpr (K >= 2) selnet<(K >= 2 ? K - 1 : 1)>(srt, CSwap{}); break;
-    case 2: if constexpr (K >= 3) selnet<(K >= 3 ? K - 2 : 1)>(srt, CSwap{}); break;
-    default: if constexpr (K >= 4) selnet<(K >= 4 ? K - 3 : 1)>(srt, CSwap{}); break;
-  }
-  float v1 = 0.f, v2 = 0.f;
-#pragma unroll
-  for (int j = 0; j < K; ++j) {
-    if (j == m1) v1 = srt[j];
-    if (j == m2) v2 = srt[j];
-  }
-  // L' = min over {j : v_j >= v_(m1)} of (v_j - e_j) <= L_m1 and H' = max over {j : v_j <= v_(m2)} of
-  // (v_j + e_j) >= H_m2 (at most m1 lower bounds can lie below the first set's minimum, and symmetrically)
-  float L = INFINITY, H = 0.f;
-#pragma unroll
-  for (int j = 0; j < K; ++j) {
-    if (j < k) {
-      const float v = fabsf(acc[j]);
-      const float ej = gam * fminf(nrm2 * colb[2 * j], n1 * colb[2 * j + 1]) + 1e-37f;
-      if (v >= v1) L = fminf(L, v - ej);
-      if (v <= v2) H = fmaxf(H, v + ej);
-    }
-  }
-  if (bad) { L = 0.f; H = INFINITY; }
-  (void)E;
-  int below = 0;
-  unsigned cmask = 0u;
-#pragma unroll
-  for (int j = 0; j < K; ++j) {
-    if (j < k) {
-      const float v = fabsf(acc[j]);
-      const float ej = gam * fminf(nrm2 * colb[2 * j], n1 * colb[2 * j + 1]) + 1e-37f;
-      if (!bad && v + ej < L) ++below;
-      else if (bad || v - ej <= H) cmask |= 1u << j;
-    }
-  }
-  const int r1 = m1 - below, r2 = m2 - below;
-  const int nc = __popc(cmask);
-  double x1 = 0.0, x2 = 0.0;
-  if (nc <= 2) {
-    const int j0 = __ffs(cmask) - 1;
-    const double c0 = tc::exact_abs_dot_sw(tile, r, M64 + j0, k, d);
-    double c1 = INFINITY;
-    if (nc == 2) c1 = tc::exact_abs_dot_sw(tile, r, M64 + (31 - __clz(cmask)), k, d);
-    const double cmin = fmin(c0, c1), cmax = fmax(c0, c1);
-    x1 = r1 == 0 ? cmin : cmax;
-    x2 = r2 == 0 ? cmin : cmax;
-  } else {
-    double ex[32];
-    int idx[32];
-    int m = 0;
-    unsigned mj = cmask;
-    while (mj) {
-      const int j = __ffs(mj) - 1;
-      mj &= mj - 1;
-      ex[m] = tc::exact_abs_dot_sw(tile, r, M64 + j, k, d);
-      idx[m++] = j;
-    }
-    for (int a = 0; a < m; ++a) {
-      int rank = 0;
-      for (int b = 0; b < m; ++b) rank += (ex[b] < ex[a]) || (ex[b] == ex[a] && idx[b] < idx[a]);
-      if (rank == r1) x1 = ex[a];
-      if (rank == r2) x2 = ex[a];
-    }
-  }
-  return (float)(0.5 * (x1 + x2));
-}
-
-template <int K>
-__global__ void __launch_bounds__(128)
-rownorm_tc_kernel(const __grid_constant__ CUtensorMap tmA, int64_t n, int d, const float* __restrict__ M32g,
-                  const double* __restrict__ M64g, const float* __restrict__ colbg, int k, float gam, int tcols,
-                  float* __restrict__ lambda, double* __restrict__ partial) {
-  extern __shared__ __align__(1024) unsigned char smraw[];
-  // 1024-B alignment by pointer arithmetic (an integer round trip would lose the shared address space)
-  unsigned char* base = smraw + ((1024u - (tc::su32(smraw) & 1023u)) & 1023u);
-  const int nch = (d + 31) >> 5;                          // 128-B K chunks
-  const int KP = nch * 32;
-  float* sA0 = (float*)base;                              // [2][nch][128][32]
-  const int tile_floats = nch * 128 * 32;
-  float* sMhi = sA0 + 2 * tile_floats;                    // [nch][32 rows][32]
-  float* sMlo = sMhi + nch * 32 * 32;
-  double* M64 = (double*)(sMlo + nch * 32 * 32);         // [k][d]
-  float* colb = (float*)(M64 + (size_t)k * d);           // [K][2]
-  __shared__ __align__(8) uint64_t bar_tma[2], bar_mma[2];
-  __shared__ uint32_t tbase;
-  __shared__ double red[4];
-  const int tid = threadIdx.x, warp = tid >> 5;
-
-  if (tid == 0) {
-    tc::mbar_init(&bar_tma[0]); tc::mbar_init(&bar_tma[1]);
-    tc::mbar_init(&bar_mma[0]); tc::mbar_init(&bar_mma[1]);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::su32(&tbase)), "r"(tcols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  // B operand: M^T (32 rows j, Kp columns l) split into hi/lo, K-major SWIZZLE_128B
-  for (int e = tid; e < 32 * KP; e += blockDim.x) {
-    const int j = e / KP, l = e - j * KP;
-    const float m = (j < K && l < d) ? M32g[l * K + j] : 0.f;
-    const float hi = tc::trunc_tf32(m), lo = m - hi;
-    const int q = l >> 5, c = (l & 31) >> 2, w = l & 3;
-    const int off = q * 32 * 32 + j * 32 + ((c ^ (j & 7)) << 2) + w;
-    sMhi[off] = hi;
-    sMlo[off] = lo;
-  }
-  for (int e = tid; e < k * d; e += blockDim.x) M64[e] = M64g[e];
-  for (int e = tid; e < 2 * K; e += blockDim.x) colb[e] = colbg[e];
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tm = tbase;
-  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-  const int per_buf = KP + 32;                            // TMEM columns: A_lo [KP] then D [32]
-  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(32 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  const int ksteps = (d + 7) >> 3;
-
-  const int64_t ntiles = (n + 127) / 128;
-  const int64_t t0 = blockIdx.x, tstep = gridDim.x;
-  if (tid == 0) {
-    if (t0 < ntiles) tc::tma_tile(sA0, &tmA, nch, (int)(t0 * 128), &bar_tma[0]);
-    if (t0 + tstep < ntiles) tc::tma_tile(sA0 + tile_floats, &tmA, nch, (int)((t0 + tstep) * 128), &bar_tma[1]);
-  }
-  unsigned ph_tma = 0u, ph_mma = 0u;   // bit b = parity of buffer b
-  float n1b[2] = {0.f, 0.f}, n2b[2] = {0.f, 0.f};
-  const int m1 = (k - 1) / 2, m2 = k / 2;
-  double local = 0.0;
-
-  // split of tile in buffer b: row tid -> A_lo into TMEM, norms; then one thread issues the MMAs
-  auto split_and_mma = [&](int b) {
-    tc::mbar_wait(&bar_tma[b], (ph_tma >> b) & 1u);
-    ph_tma ^= 1u << b;
-    const float* tile = sA0 + b * tile_floats;
-    float s1 = 0.f, s2 = 0.f;
-    for (int q = 0; q < nch; ++q) {
-      uint32_t lo[32];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const float4 v = *(const float4*)(tile + q * 128 * 32 + tid * 32 + ((c ^ (tid & 7)) << 2));
-        const float a[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          s1 += fabsf(a[w]);
-          s2 = fmaf(a[w], a[w], s2);
-          lo[c * 4 + w] = __float_as_uint(a[w] - tc::trunc_tf32(a[w]));
-        }
-      }
-      tc::st32(tm + lane_off + (uint32_t)(b * per_buf + q * 32), lo);
-    }
-    if (b == 0) { n1b[0] = s1; n2b[0] = s2; } else { n1b[1] = s1; n2b[1] = s2; }
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t tD = tm + (uint32_t)(b * per_buf + KP);
-      int cnt = 0;
-      for (int pass = 0; pass < 3; ++pass) {
-        const float* Bm = pass == 1 ? sMlo : sMhi;
-        for (int ks = 0; ks < ksteps; ++ks) {
-          const int q = ks >> 2, kin = ks & 3;
-          const uint64_t bd = tc::sdesc((const unsigned char*)(Bm + q * 32 * 32) + kin * 32);
-          const uint32_t acc = cnt > 0 ? 1u : 0u;
-          if (pass < 2) {
-            const uint64_t ad = tc::sdesc((const unsigned char*)(tile + q * 128 * 32) + kin * 32);
-            asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
-                         ::"r"(tD), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
-          } else {
-            const uint32_t ta = tm + (uint32_t)(b * per_buf + ks * 8);
-            asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n"
-                         ::"r"(tD), "r"(ta), "l"(bd), "r"(idesc), "r"(acc));
-          }
-          ++cnt;
-        }
-      }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(tc::su32(&bar_mma[b]))
-                   : "memory");
-    }
-  };
-
-  if (t0 < ntiles) split_and_mma(0);
-  int i = 0;
-  for (int64_t t = t0; t < ntiles; t += tstep, ++i) {
-    const int b = i & 1, nb = b ^ 1;
-    if (t + tstep < ntiles) split_and_mma(nb);
-    tc::mbar_wait(&bar_mma[b], (ph_mma >> b) & 1u);
-    ph_mma ^= 1u << b;
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    uint32_t dv[32];
-    tc::ld32(tm + lane_off + (uint32_t)(b * per_buf + KP), dv);
-    float acc[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) acc[j] = __uint_as_float(dv[j]);
-    const int64_t row = t * 128 + tid;
-    const float n1 = b ? n1b[1] : n1b[0], n2 = b ? n2b[1] : n2b[0];
-    if (row < n) {
-      const float lam = certified_median_tc<K>(acc, n1, n2, colb, gam, k, m1, m2, sA0 + b * tile_floats, tid, d, M64);
-      lambda[row] = lam;
-      local += (double)lam;
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();   // buffer b (smem tile, TMEM A_lo and D) is free
-    if (tid == 0 && t + 2 * tstep < ntiles)
-      tc::tma_tile(sA0 + b * tile_floats, &tmA, nch, (int)((t + 2 * tstep) * 128), &bar_tma[b]);
-  }
-  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
-  if ((tid & 31) == 0) red[warp] = local;
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (tid == 0) partial[blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(tcols));
-}
 
 // ------------------------------------------------------------------------------------------------
 // ws: warp-specialised tcgen05 row-norm (one persistent CTA per SM, 16 warps).
@@ -1085,44 +835,6 @@ bool tc_ok(const float* A, int64_t n, int d, int64_t lda) {
 }
 
 template <int K>
-fct_status launch_tc(const float* A, int64_t n, int d, int64_t lda, const float* M32, const double* M64,
-                     const float* colb, int k, float* lambda, double* partial, int grid, cudaStream_t st) {
-  CUtensorMap map;
-  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)n};
-  cuuint64_t strides[1] = {(cuuint64_t)lda * sizeof(float)};
-  cuuint32_t box[2] = {32, 128};
-  cuuint32_t es[2] = {1, 1};
-  CUresult cr = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)A, dims, strides, box, es,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  FCT_CHECK_ARG(cr == CUDA_SUCCESS, FCT_ERR_CUDA, "l1_rownorm: cuTensorMapEncodeTiled failed (%d)", (int)cr);
-  const int nch = (d + 31) / 32;
-  const int per_buf = nch * 32 + 32;
-  int tcols = 32;
-  while (tcols < 2 * per_buf) tcols <<= 1;
-  const size_t smem = 1024 + sizeof(float) * (2 * (size_t)nch * 128 * 32 + 2 * (size_t)nch * 32 * 32) +
-                      sizeof(double) * (size_t)k * d + sizeof(float) * 2 * K;
-  auto kern = rownorm_tc_kernel<K>;
-  FCT_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  FCT_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  // residency from the shared-memory and TMEM budgets (the occupancy API under-reports for this
-  // tcgen05 kernel: ncu shows 2 resident CTAs at 97 KB while the API returns 1)
-  int dev = 0, smem_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-  int occ = std::max(1, (int)((size_t)smem_sm / (smem + 2048)));
-  occ = std::max(1, std::min(occ, 512 / tcols));
-  const int g = std::max(1, std::min(grid, fct::num_sms() * occ));
-  if (fct::debug_sync()) fprintf(stderr, "[fct] rownorm_tc: grid %d occ %d tcols %d smem %zu\n", g, occ, tcols, smem);
-  // error bound of the 3xTF32 evaluation (measured 1.9e-6 on B200; 2^-14 leaves a 30x margin)
-  const float gam = 6.103515625e-05f * 1.05f;
-  FCT_CUDA_RET(cudaMemsetAsync(partial, 0, sizeof(double) * grid, st));
-  kern<<<g, 128, smem, st>>>(map, n, d, M32, M64, colb, k, gam, tcols, lambda, partial);
-  FCT_LAUNCHED("rownorm_tc_kernel", st);
-  return FCT_OK;
-}
-
-template <int K>
 fct_status launch_ws(const float* A, int64_t n, int d, int64_t lda, const float* M32, const double* M64,
                      const float* colb, int k, float* lambda, double* partial, int grid, cudaStream_t st) {
   CUtensorMap map;
@@ -1147,7 +859,7 @@ fct_status launch_ws(const float* A, int64_t n, int d, int64_t lda, const float*
   FCT_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int g = std::max(1, std::min(grid, fct::num_sms()));
   if (fct::debug_sync()) fprintf(stderr, "[fct] rownorm_ws: grid %d NA %d ND %d smem %zu\n", g, NA, ND, smem);
-  const float gam = 6.103515625e-05f * 1.05f;   // 3xTF32 bound (see rownorm_tc_kernel)
+  const float gam = 6.103515625e-05f * 1.05f;   // 3xTF32 bound (see the tc helpers above)
   FCT_CUDA_RET(cudaMemsetAsync(partial, 0, sizeof(double) * grid, st));
   kern<<<g, wsk::kThreads, smem, st>>>(map, A, n, d, lda, M32, M64, colb, k, gam, NA, ND, lambda, partial);
   FCT_LAUNCHED("rownorm_ws_kernel", st);
@@ -1157,13 +869,14 @@ fct_status launch_ws(const float* A, int64_t n, int d, int64_t lda, const float*
 template <int K>
 fct_status launch_rownorm(const float* A, int64_t n, int d, int64_t lda, const float* M32, const double* M64,
                           const float* colb, int k, float* lambda, double* partial, int grid, cudaStream_t st) {
-  if (tc_ok(A, n, d, lda) && !getenv("FCT_ROWNORM_TC1")) {
+  // dispatch: ws2 (instances for the configurations' k) -> ws (any k; tcgen05) -> v1 / SIMT (unaligned A,
+  // d % 4 != 0, d > 128, or a shared-memory budget ws cannot meet)
+  if (tc_ok(A, n, d, lda)) {
     const fct_status r2 = fct_rownorm_ws2(A, n, d, lda, M32, K, M64, colb, k, partial, grid, lambda, st);
     if (r2 != FCT_ERR_UNSUPPORTED) return r2;
     const fct_status r = launch_ws<K>(A, n, d, lda, M32, M64, colb, k, lambda, partial, grid, st);
     if (r != FCT_ERR_UNSUPPORTED) return r;
   }
-  if (tc_ok(A, n, d, lda)) return launch_tc<K>(A, n, d, lda, M32, M64, colb, k, lambda, partial, grid, st);
   const float u = 5.9604645e-08f;  // 2^-24
   const float gam1 = (float)(d + 3) * u * 1.1f;
   if (v1_ok(A, d, lda, k, K)) {
