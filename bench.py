@@ -86,6 +86,26 @@ def read_only_ceiling_gbs(nbytes=4 << 30):
     return best
 
 
+def h2d_ceiling_gbs(nbytes=1 << 30):
+    """A live pinned host -> device copy on this GPU (1 GiB, best of 3, CUDA events): the ceiling of the e2e path."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    g = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    g.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.copy_(h, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    del h, g
+    torch.cuda.empty_cache()
+    return best
+
+
 def workload_desc(cfg, n_total):
     kinds = {1: "i.i.d. N(0,1)", 2: "N(0,1) features + planted l1 regression column -b",
              3: "N(0,1) rows x min(|Cauchy|^0.5, 1e4)", 4: "N(0,1), 1% of rows x1e3",
@@ -405,6 +425,10 @@ def main():
                "d2h_bytes_per_step": int(d2h), "ms_per_step": te, "steps": args.e2e_steps,
                "path": "fct_pipeline_host (C ABI, pinned host buffers)"}
         del H, hA
+        hc_gbs = h2d_ceiling_gbs()
+        e2e["h2d_gbs"] = h2d / (te * 1e-3) / 1e9
+        e2e["h2d_ceiling_gbs"] = hc_gbs
+        e2e["frac_of_h2d_ceiling"] = e2e["h2d_gbs"] / hc_gbs
 
     # ---- e2e at N > 1 through the public multi-GPU API: every step copies the rank's shard from pinned host
     # memory, runs dist.run_step (collectives included) and reads its samples back; max over ranks
