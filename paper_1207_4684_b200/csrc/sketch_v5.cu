@@ -437,6 +437,26 @@ fct_status launch_v5(const float* A, int64_t nfull, int64_t d, int64_t lda, cons
   int64_t ngrp = (int64_t)fct::num_sms() / nslices;
   const int64_t min_grp = (2 * nblocks * (int64_t)s + 2048LL * r1 - 1) / (2048LL * r1);
   ngrp = std::max<int64_t>(std::max<int64_t>(ngrp, 1), min_grp);
+  // One wave leaves SMs idle when neither the groups nor the extra CTAs below fill them (cfg 5: 25 slices, 5 groups
+  // + 5 extra CTAs = 130 of 148 SMs), and min_grp can force several waves (cfg 5 at 2^26 rows and more). Then run
+  // several waves of one CTA per SM, unpaced, with the smallest group count >= max(min_grp, 4 waves' worth) whose
+  // last wave is >= 98 % full. Measured (tools/ngrp_sweep.sh, profiles/r02_sketch_ngrp_sweep.jsonl): cfg-5 shard
+  // 2^25 rows 11.75 -> 10.18 ms, cfg 5 2^28 rows 87.7 -> 81.6 ms; cfg 4 (one full wave) 9.18 vs 9.13-9.22 ms.
+  {
+    const int64_t nsm = fct::num_sms();
+    int64_t left = nsm - ngrp * nslices, ne = left;
+    while (ne > 0 && nslices % ne) --ne;
+    const bool one_wave_full = left >= 0 && (ngrp * nslices + ne) * 100 >= nsm * 95;
+    if (!one_wave_full && !getenv("FCT_SKETCH_ONEWAVE")) {
+      int64_t g = std::max<int64_t>(min_grp, (4 * nsm + nslices - 1) / nslices);
+      for (int64_t t = g; t < g + 2 * nsm; ++t) {
+        const int64_t ctas = t * nslices, waves = (ctas + nsm - 1) / nsm;
+        if (ctas * 100 >= waves * nsm * 98) { g = t; break; }
+      }
+      ngrp = g;
+    }
+  }
+  if (const char* e = getenv("FCT_SKETCH_NGRP")) ngrp = std::max<int64_t>(min_grp, atoll(e));   // sweep override
   ngrp = std::min<int64_t>(ngrp, (nblocks + TL - 1) / TL);
   if (ngrp < 1) ngrp = 1;
   if (ngrp * nslices > fct::num_sms()) pace = nullptr;

@@ -94,6 +94,20 @@ def test_sketch_extra_ctas_tail(fct, noextra, monkeypatch):
     assert_sketch_close(Yg, Yo, Mb)
 
 
+@pytest.mark.parametrize("onewave", [False, True])
+def test_sketch_multiwave_grid(fct, onewave, monkeypatch):
+    """K1's multi-wave grid: 19 slices of 4 columns (d = 76, r1 = 8192) fill only 134 of 148 SMs in one wave, so
+    the launch runs several unpaced waves of one CTA per SM (capped here by the 48 blocks); FCT_SKETCH_ONEWAVE=1
+    keeps the paced single wave with its extra CTA. Ragged tail block included."""
+    if onewave:
+        monkeypatch.setenv("FCT_SKETCH_ONEWAVE", "1")
+    cfg = fctgen.CONFIGS[5]
+    inp = fctgen.make_inputs(cfg, n=48 * 1024 + 33, s=1024, r1=8192, d=76)
+    Yo, Mb = oracle.sketch(inp.A, inp.signs, inp.cauchy, inp.hash, 1024, 8192)
+    Yg = sketch_gpu(fct, inp)
+    assert_sketch_close(Yg, Yo, Mb)
+
+
 def test_sketch_strided_accumulate_and_shards(fct):
     """lda > d (a column slice of a wider matrix), accumulate=1, and s-aligned row shards."""
     cfg = fctgen.CONFIGS[2]
